@@ -1,0 +1,230 @@
+/*
+ * pbn_b200.h — C-ABI of the B200-native PBN trajectory engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arxiv 1605.00854 artifact, /root/reference/proj):
+ *
+ *   reference interface (header-level C++ templates)          replaced by
+ *   ----------------------------------------------------------  ---------------------------
+ *   pbn::parse_model            io.hpp:74-197                   pbn_model_parse
+ *   pbn::serialize_model        io.hpp:205-226                  pbn_model_serialize
+ *   pbn::validate               model.hpp:81-117                (inside pbn_model_parse)
+ *   pbn::reduce / find_leaves   reduction.hpp:28-94             pbn_prepare (+ pbn_plan_reduced)
+ *   pbn::perturbation_plan::build perturbation.hpp:25-43        pbn_prepare
+ *   pbn::partition / combine    grouping.hpp:102-308            pbn_prepare
+ *   pbn::prepare                engine.hpp:85-164               pbn_prepare + pbn_plan_get_view
+ *   pbn::compile_predicate      engine.hpp:357-362              pbn_compile_predicate
+ *   pbn::grouped_simulator::step engine.hpp:255-312  ┐
+ *   pbn::simulate               engine.hpp:371-384  ┘           pbn_gpu_run / pbn_gpu_run_device
+ *   pbn::estimate_steady_state  estimator.hpp:137-244           pbn_estimate (pooled ensemble)
+ *
+ * Conventions (mirroring the reference):
+ *   - No C++ exception crosses this boundary. Every call returns a status code;
+ *     the reference's exception classes map to the CLI's exit codes
+ *     (errors.hpp:10-32, pbn_main.cpp:302-311):
+ *       PBN_OK=0, PBN_EUSAGE=1, PBN_EMODEL=2 (model_error/parse_error),
+ *       PBN_ERESOURCE=3 (resource_error), PBN_ECUDA=4 (device failure).
+ *     pbn_last_error() returns the message of the last failure on this thread.
+ *   - The plan is immutable after pbn_prepare and may be shared by threads
+ *     (SPEC.md:411). A device handle (pbn_gpu) is used by one host thread.
+ *   - States are bit-packed in ENGINE bit order, exactly the reference's
+ *     `pbn::state` words (bitstate.hpp:12-99): bit i lives in 64-bit word i/64,
+ *     each trajectory owns pbn_state_words(n_kept) = n_kept/64 + 1 words (the
+ *     last one carries the always-zero slack bit).
+ *   - Randomness is the injected counter-based stream described in DESIGN.md:
+ *     Philox4x32-10, key = seed, counter = (trajectory, draw block, step).
+ *     Draw d of step s of trajectory tau is a function of (seed, tau, s, d)
+ *     only, so results are identical for any device count / launch split.
+ */
+#ifndef PBN_B200_H
+#define PBN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBN_OK 0
+#define PBN_EUSAGE 1
+#define PBN_EMODEL 2
+#define PBN_ERESOURCE 3
+#define PBN_ECUDA 4
+
+/* Random stream kinds (how a Philox block is cut into next_double() values). */
+#define PBN_STREAM_U53 0 /* 2 draws per Philox block: ((x[2e+1]<<32|x[2e]) >> 11) * 2^-53, as rng.hpp:35 */
+#define PBN_STREAM_U32 1 /* 4 draws per Philox block: x[e] * 2^-32 (fast stream)                      */
+
+/* Per-trajectory statistics record, PBN_COUNT_FIELDS uint64 each. */
+#define PBN_COUNT_FIELDS 8
+#define PBN_C_STEPS 0      /* steps simulated in this call                                   */
+#define PBN_C_HITS 1       /* steps whose post-step state satisfies the predicate (engine.hpp:380) */
+#define PBN_C_T00 2        /* predicate-process transitions prev->cur: 0->0                 */
+#define PBN_C_T01 3        /*                                          0->1                 */
+#define PBN_C_T10 4        /*                                          1->0                 */
+#define PBN_C_T11 5        /*                                          1->1                 */
+#define PBN_C_FNSTEPS 6    /* steps that ran the function phase (no kept flip, leaf check passed) */
+#define PBN_C_PERTSTEPS 7  /* steps with at least one kept-node flip (engine.hpp:267)        */
+
+/* Run flags. */
+#define PBN_RUN_NODE_COUNTS 1u /* also accumulate per-bit one-counts (engine.hpp:378-379) */
+
+/* Opaque handles. */
+typedef struct pbn_model pbn_model; /* parsed + validated model           (model.hpp:57-69)  */
+typedef struct pbn_plan pbn_plan;   /* prepared simulation (flat plan)    (engine.hpp:22-79) */
+typedef struct pbn_gpu pbn_gpu;     /* device-resident encoded plan                           */
+
+/*
+ * Flat view of a prepared simulation: the hot-loop arrays of the reference's
+ * prepared_simulation (engine.hpp:22-79), one plain array per field.
+ * Any producer may fill it — pbn_plan_get_view() for plans built by this
+ * library, or a reference-side shim over pbn::prepared_simulation
+ * — and pbn_gpu_create() accepts either.
+ */
+typedef struct pbn_plan_view {
+  uint32_t n_kept;          /* reduced node count n'                       (engine.hpp:75)   */
+  double t;                 /* leaf no-perturb probability (1-p)^l         (reduction.hpp:91) */
+  /* perturbation plan (perturbation.hpp:16-44) */
+  uint32_t pert_groups;     /* g                                                            */
+  uint32_t pert_k;          /* k                                                            */
+  uint32_t pert_k_prime;    /* k'                                                           */
+  uint32_t pert_size;       /* 2^k alias cells                                              */
+  uint64_t pert_mask;       /* 2^k' - 1                                                     */
+  const double* pert_cut;   /* [pert_size] alias cut-offs                  (alias.hpp:95)    */
+  const uint32_t* pert_alias; /* [pert_size] alias targets                 (alias.hpp:96)    */
+  /* groups in engine order (engine.hpp:29-36) */
+  uint32_t n_groups;
+  const uint32_t* grp_offset;      /* [n_groups] cum[i]                                      */
+  const uint32_t* grp_fn_begin;    /* [n_groups] first combined function in fns              */
+  const uint32_t* grp_alias_begin; /* [n_groups] into alias_cut / alias_idx                  */
+  const uint32_t* grp_alias_size;  /* [n_groups] 0 when the group has one combined function  */
+  /* flattened group alias tables (engine.hpp:40-41) */
+  uint64_t n_alias;
+  const double* alias_cut;
+  const uint32_t* alias_idx;
+  /* combined functions (engine.hpp:52-63) */
+  uint32_t n_fns;
+  const uint64_t* fn_gather_begin; /* [n_fns] into fn_gather                                 */
+  const uint64_t* fn_table_begin;  /* [n_fns] into fn_tables, 2^gather_count entries         */
+  const uint32_t* fn_gather_count; /* [n_fns]                                                */
+  uint64_t n_gather;
+  const uint32_t* fn_gather;       /* engine bit positions, lists padded to >= 8 with n_kept */
+  uint64_t n_table;
+  const uint64_t* fn_tables;       /* packed member outputs (member 0 = bit 0)               */
+} pbn_plan_view;
+
+/* BASELINE-shaped synthetic network. */
+typedef struct pbn_gen_params {
+  uint32_t n;              /* nodes                                                         */
+  uint32_t f_min, f_max;   /* predictor functions per node ~ U{f_min..f_max}                */
+  uint32_t p_min, p_max;   /* parents per function ~ U{p_min..p_max} (distinct, sorted)     */
+  double leaf_frac;        /* designated leaves (never drawn as parents)                    */
+  double perturbation;     /* p                                                             */
+  uint32_t n_targets;      /* interest / predicate nodes (never designated leaves)          */
+  uint32_t targets_fixed;  /* 1: targets are nodes 0..n_targets-1 with value 1 (config 1)   */
+  uint64_t seed;
+} pbn_gen_params;
+
+/* Run arguments of one ensemble launch. */
+typedef struct pbn_run_args {
+  uint64_t seed;
+  uint64_t traj_begin;   /* global id of the first trajectory (keys the stream)            */
+  uint32_t n_traj;
+  uint32_t stream;       /* PBN_STREAM_*                                                   */
+  uint64_t step_begin;   /* global index of the first step (resumable runs)                */
+  uint64_t n_steps;
+  const uint32_t* pred_bits;  /* engine bits of the predicate terms (host)                 */
+  const uint8_t* pred_vals;   /* wanted values                                              */
+  uint32_t n_pred;            /* 0 = no predicate (hits/transitions stay 0)                */
+  uint32_t flags;             /* PBN_RUN_*                                                  */
+} pbn_run_args;
+
+/* ---- errors / library info ------------------------------------------------- */
+const char* pbn_last_error(void);
+const char* pbn_version(void);
+uint32_t pbn_state_words(uint32_t n_kept); /* n_kept/64 + 1 (bitstate.hpp:19) */
+
+/* ---- model (io.hpp / model.hpp / own generator) ---------------------------- */
+int pbn_model_parse(const char* text, size_t len, pbn_model** out);
+int pbn_model_serialize(const pbn_model* m, char* buf, size_t cap, size_t* len_out);
+int pbn_model_generate(const pbn_gen_params* gp, pbn_model** out, uint32_t* pred_nodes,
+                       uint8_t* pred_vals, uint32_t* n_pred_out);
+int pbn_model_info(const pbn_model* m, uint32_t* n, double* p, uint32_t* n_interest,
+                   double* density);
+int pbn_model_node_index(const pbn_model* m, const char* name, uint32_t* index_out);
+void pbn_model_free(pbn_model* m);
+
+/* ---- preparation (reduction.hpp, perturbation.hpp, grouping.hpp, engine.hpp:85) ---- */
+int pbn_prepare(const pbn_model* m, uint64_t theta, uint32_t k_max, uint32_t max_group_parents,
+                pbn_plan** out);
+int pbn_plan_get_view(const pbn_plan* plan, pbn_plan_view* view); /* valid while plan lives */
+/* Reduction bookkeeping: original n, removed count, index_map[n] (-1 removed),
+ * engine_pos[n_kept] (reduced index -> engine bit). Arrays may be NULL. */
+int pbn_plan_reduced(const pbn_plan* plan, uint32_t* original_n, uint32_t* n_removed,
+                     int32_t* index_map, uint32_t* engine_pos, uint32_t* removed);
+/* Group membership in engine order: members[n_kept] (reduced indices), cum[n_groups+1]. */
+int pbn_plan_groups(const pbn_plan* plan, uint32_t* members, uint32_t* cum);
+/* Predicate over ORIGINAL node indices -> engine bits (engine.hpp:357-362). */
+int pbn_compile_predicate(const pbn_plan* plan, const uint32_t* nodes, const uint8_t* vals,
+                          uint32_t n, uint32_t* engine_bits_out);
+void pbn_plan_free(pbn_plan* plan);
+
+/* ---- device engine ---------------------------------------------------------- */
+int pbn_device_count(int* count);
+/* Encode + upload a plan. lanes_per_traj: 0 = choose automatically, else 1,2,4,8,16,32. */
+int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lanes_per_traj,
+                   pbn_gpu** out);
+/* Force where the plan lives: 0 auto, 1 global (L1/L2), 2 core in smem + tables
+ * global, 3 everything in smem. PBN_ERESOURCE if it does not fit. */
+int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement);
+int pbn_gpu_info(const pbn_gpu* g, uint32_t* lanes_per_traj, uint32_t* tables_in_smem,
+                 uint64_t* smem_bytes, uint64_t* plan_bytes, uint32_t* warps_per_cta);
+/* End-to-end: HOST buffers. states_inout: n_traj * pbn_state_words(n_kept) uint64,
+ * counts_out: n_traj * PBN_COUNT_FIELDS uint64, node_counts_out (flag NODE_COUNTS):
+ * n_traj * n_kept uint64 or NULL. Synchronous. */
+int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states_inout, uint64_t* counts_out,
+                uint64_t* node_counts_out);
+/* Device-resident: DEVICE pointers, asynchronous on `stream` (a cudaStream_t, 0 = legacy). */
+int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states,
+                       uint64_t* d_counts, uint64_t* d_node_counts, void* stream);
+/* Stream known-answer hook: n Philox4x32-10 blocks of (4 x u32 counters) under key
+ * = seed, computed by the device's Philox (tests compare with the oracle's). */
+int pbn_philox_kat(const uint32_t* ctr, uint32_t n, uint64_t seed, uint32_t* out);
+/* Launch count of the last run call (kernels launched). */
+uint32_t pbn_gpu_last_launches(const pbn_gpu* g);
+void pbn_gpu_destroy(pbn_gpu* g);
+
+/* ---- pooled ensemble steady-state estimate (estimator.hpp:137-244) ---------- */
+typedef struct pbn_estimate_request {
+  double precision;          /* r       (estimator.hpp:60) */
+  double confidence;         /* 0.95    (estimator.hpp:61) */
+  uint64_t pilot;            /* per-trajectory pilot steps (estimator.hpp:62) */
+  double burn_epsilon;       /* 0 -> precision (estimator.hpp:63) */
+  uint32_t max_refinements;  /* (estimator.hpp:64) */
+  double sample_inflation;   /* 1.3 (estimator.hpp:68) */
+  uint64_t seed;
+  uint64_t traj_begin;
+  uint32_t n_traj;
+  uint32_t stream;
+} pbn_estimate_request;
+
+typedef struct pbn_estimate_result {
+  double estimate;
+  uint64_t sample_size_used; /* pooled recorded samples over all trajectories */
+  uint64_t burn_in_used;     /* per trajectory */
+  uint64_t steps_per_traj;   /* total steps simulated per trajectory */
+  uint32_t kappa;
+  uint32_t degenerate;
+  double alpha, beta;
+  double wall_seconds;
+} pbn_estimate_result;
+
+int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pred_bits,
+                 const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
+                 pbn_estimate_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBN_B200_H */

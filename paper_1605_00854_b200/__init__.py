@@ -1,0 +1,431 @@
+"""pbn_b200 — B200-native PBN trajectory engine (arxiv 1605.00854 hot path).
+
+Python mirror of the reference's host interface over the C-ABI in
+``include/pbn_b200.h`` (``libpbn_b200.so``, built in-tree). Names follow the
+reference (``/root/reference/proj/include/pbn``):
+
+==============================  =================================================
+reference                       here
+==============================  =================================================
+``parse_model`` io.hpp:74       :func:`parse_model` -> :class:`Model`
+``serialize_model`` io.hpp:205  :meth:`Model.serialize`
+``prepare`` engine.hpp:85       :func:`prepare` -> :class:`PreparedSimulation`
+``compile_predicate`` :357      :meth:`PreparedSimulation.compile_predicate`
+``simulate`` engine.hpp:371     :meth:`GpuEnsemble.simulate` (ensemble of trajectories)
+==============================  =================================================
+
+Errors mirror the reference's exception classes (errors.hpp:10-32):
+:class:`ModelError` (exit code 2), :class:`ResourceError` (3); device
+failures raise :class:`CudaError`. There is no CPU fallback: if the shared
+library is missing, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpbn_b200.so")
+
+STREAM_U53 = 0
+STREAM_U32 = 1
+COUNT_FIELDS = 8
+C_STEPS, C_HITS, C_T00, C_T01, C_T10, C_T11, C_FNSTEPS, C_PERTSTEPS = range(8)
+DEFAULT_THETA = 1 << 25  # engine.hpp:81
+DEFAULT_K = 16  # engine.hpp:82
+DEFAULT_MGP = 18  # engine.hpp:83
+
+
+class PbnError(RuntimeError):
+    code = 1
+
+
+class UsageError(PbnError):
+    code = 1
+
+
+class ModelError(PbnError):
+    code = 2
+
+
+class ResourceError(PbnError):
+    code = 3
+
+
+class CudaError(PbnError):
+    code = 4
+
+
+_ERRORS = {1: UsageError, 2: ModelError, 3: ResourceError, 4: CudaError}
+
+
+class PlanView(C.Structure):
+    _fields_ = [
+        ("n_kept", C.c_uint32), ("t", C.c_double),
+        ("pert_groups", C.c_uint32), ("pert_k", C.c_uint32), ("pert_k_prime", C.c_uint32),
+        ("pert_size", C.c_uint32), ("pert_mask", C.c_uint64),
+        ("pert_cut", C.POINTER(C.c_double)), ("pert_alias", C.POINTER(C.c_uint32)),
+        ("n_groups", C.c_uint32),
+        ("grp_offset", C.POINTER(C.c_uint32)), ("grp_fn_begin", C.POINTER(C.c_uint32)),
+        ("grp_alias_begin", C.POINTER(C.c_uint32)), ("grp_alias_size", C.POINTER(C.c_uint32)),
+        ("n_alias", C.c_uint64), ("alias_cut", C.POINTER(C.c_double)),
+        ("alias_idx", C.POINTER(C.c_uint32)),
+        ("n_fns", C.c_uint32), ("fn_gather_begin", C.POINTER(C.c_uint64)),
+        ("fn_table_begin", C.POINTER(C.c_uint64)), ("fn_gather_count", C.POINTER(C.c_uint32)),
+        ("n_gather", C.c_uint64), ("fn_gather", C.POINTER(C.c_uint32)),
+        ("n_table", C.c_uint64), ("fn_tables", C.POINTER(C.c_uint64)),
+    ]
+
+
+class GenParams(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint32), ("f_min", C.c_uint32), ("f_max", C.c_uint32),
+        ("p_min", C.c_uint32), ("p_max", C.c_uint32), ("leaf_frac", C.c_double),
+        ("perturbation", C.c_double), ("n_targets", C.c_uint32),
+        ("targets_fixed", C.c_uint32), ("seed", C.c_uint64),
+    ]
+
+
+class RunArgs(C.Structure):
+    _fields_ = [
+        ("seed", C.c_uint64), ("traj_begin", C.c_uint64), ("n_traj", C.c_uint32),
+        ("stream", C.c_uint32), ("step_begin", C.c_uint64), ("n_steps", C.c_uint64),
+        ("pred_bits", C.POINTER(C.c_uint32)), ("pred_vals", C.POINTER(C.c_uint8)),
+        ("n_pred", C.c_uint32), ("flags", C.c_uint32),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, U32, U64, I = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+    sig = {
+        "pbn_last_error": (C.c_char_p, []),
+        "pbn_version": (C.c_char_p, []),
+        "pbn_state_words": (U32, [U32]),
+        "pbn_model_parse": (I, [C.c_char_p, C.c_size_t, C.POINTER(P)]),
+        "pbn_model_serialize": (I, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "pbn_model_generate": (I, [C.POINTER(GenParams), C.POINTER(P), C.POINTER(U32),
+                                   C.POINTER(C.c_uint8), C.POINTER(U32)]),
+        "pbn_model_info": (I, [P, C.POINTER(U32), C.POINTER(C.c_double), C.POINTER(U32),
+                               C.POINTER(C.c_double)]),
+        "pbn_model_node_index": (I, [P, C.c_char_p, C.POINTER(U32)]),
+        "pbn_model_free": (None, [P]),
+        "pbn_prepare": (I, [P, U64, U32, U32, C.POINTER(P)]),
+        "pbn_plan_get_view": (I, [P, C.POINTER(PlanView)]),
+        "pbn_plan_reduced": (I, [P, C.POINTER(U32), C.POINTER(U32), C.POINTER(C.c_int32),
+                                 C.POINTER(U32), C.POINTER(U32)]),
+        "pbn_plan_groups": (I, [P, C.POINTER(U32), C.POINTER(U32)]),
+        "pbn_compile_predicate": (I, [P, C.POINTER(U32), C.POINTER(C.c_uint8), U32,
+                                      C.POINTER(U32)]),
+        "pbn_plan_free": (None, [P]),
+        "pbn_device_count": (I, [C.POINTER(I)]),
+        "pbn_gpu_create": (I, [C.POINTER(PlanView), I, U32, C.POINTER(P)]),
+        "pbn_gpu_set_placement": (I, [P, U32]),
+        "pbn_gpu_info": (I, [P, C.POINTER(U32), C.POINTER(U32), C.POINTER(U64), C.POINTER(U64),
+                             C.POINTER(U32)]),
+        "pbn_gpu_run": (I, [P, C.POINTER(RunArgs), C.POINTER(U64), C.POINTER(U64),
+                            C.POINTER(U64)]),
+        "pbn_gpu_run_device": (I, [P, C.POINTER(RunArgs), P, P, P, P]),
+        "pbn_gpu_last_launches": (U32, [P]),
+        "pbn_gpu_destroy": (None, [P]),
+        "pbn_philox_kat": (I, [C.POINTER(U32), U32, U64, C.POINTER(U32)]),
+        "pbn_estimate": (I, [P, P, P, P, U32, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+EXPORTED_SYMBOLS = (
+    "pbn_last_error", "pbn_version", "pbn_state_words", "pbn_model_parse", "pbn_model_serialize",
+    "pbn_model_generate", "pbn_model_info", "pbn_model_node_index", "pbn_model_free", "pbn_prepare",
+    "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
+    "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
+    "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_destroy", "pbn_estimate",
+)
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib.pbn_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, PbnError)(msg)
+
+
+def _u32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _u64p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def state_words(n_kept: int) -> int:
+    """Words per trajectory state (bitstate.hpp:19: n/64 + 1, one slack word)."""
+    return n_kept // 64 + 1
+
+
+# ----------------------------------------------------------------------------
+class Model:
+    """Parsed, validated PBN (model.hpp:57-69)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.pbn_model_free(self._h)
+            self._h = C.c_void_p(None)
+
+    def serialize(self) -> str:
+        n = C.c_size_t(0)
+        _check(lib.pbn_model_serialize(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.pbn_model_serialize(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.raw[: n.value].decode()
+
+    def info(self):
+        n, ni = C.c_uint32(), C.c_uint32()
+        p, d = C.c_double(), C.c_double()
+        _check(lib.pbn_model_info(self._h, C.byref(n), C.byref(p), C.byref(ni), C.byref(d)))
+        return {"n": n.value, "p": p.value, "n_interest": ni.value, "density": d.value}
+
+    @property
+    def n(self) -> int:
+        return self.info()["n"]
+
+    def node_index(self, name: str) -> int:
+        out = C.c_uint32()
+        _check(lib.pbn_model_node_index(self._h, name.encode(), C.byref(out)))
+        return out.value
+
+
+def parse_model(text: str) -> Model:
+    """io.hpp:74-197: parse + validate a PBN text model."""
+    h = C.c_void_p()
+    raw = text.encode()
+    _check(lib.pbn_model_parse(raw, len(raw), C.byref(h)))
+    return Model(h.value)
+
+
+def generate_model(n, f_range, p_range, p, leaf_frac=0.0, n_targets=2, targets_fixed=False,
+                   seed=1605):
+    """BASELINE-shaped synthetic network. Returns (model, predicate terms)."""
+    gp = GenParams(n, f_range[0], f_range[1], p_range[0], p_range[1], leaf_frac, p, n_targets,
+                   1 if targets_fixed else 0, seed)
+    h = C.c_void_p()
+    nodes = (C.c_uint32 * max(1, n_targets))()
+    vals = (C.c_uint8 * max(1, n_targets))()
+    cnt = C.c_uint32()
+    _check(lib.pbn_model_generate(C.byref(gp), C.byref(h), nodes, vals, C.byref(cnt)))
+    return Model(h.value), [(int(nodes[i]), int(vals[i])) for i in range(cnt.value)]
+
+
+def _arr(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+
+@dataclass
+class FlatPlan:
+    """Copy of the flat hot-loop arrays (engine.hpp:22-79)."""
+
+    n_kept: int
+    t: float
+    pert_groups: int
+    pert_k: int
+    pert_k_prime: int
+    pert_mask: int
+    pert_cut: np.ndarray
+    pert_alias: np.ndarray
+    grp_offset: np.ndarray
+    grp_fn_begin: np.ndarray
+    grp_alias_begin: np.ndarray
+    grp_alias_size: np.ndarray
+    alias_cut: np.ndarray
+    alias_idx: np.ndarray
+    fn_gather_begin: np.ndarray
+    fn_table_begin: np.ndarray
+    fn_gather_count: np.ndarray
+    fn_gather: np.ndarray
+    fn_tables: np.ndarray
+
+    @staticmethod
+    def from_view(v: PlanView) -> "FlatPlan":
+        return FlatPlan(
+            v.n_kept, v.t, v.pert_groups, v.pert_k, v.pert_k_prime, v.pert_mask,
+            _arr(v.pert_cut, v.pert_size, np.float64), _arr(v.pert_alias, v.pert_size, np.uint32),
+            _arr(v.grp_offset, v.n_groups, np.uint32), _arr(v.grp_fn_begin, v.n_groups, np.uint32),
+            _arr(v.grp_alias_begin, v.n_groups, np.uint32),
+            _arr(v.grp_alias_size, v.n_groups, np.uint32),
+            _arr(v.alias_cut, v.n_alias, np.float64), _arr(v.alias_idx, v.n_alias, np.uint32),
+            _arr(v.fn_gather_begin, v.n_fns, np.uint64), _arr(v.fn_table_begin, v.n_fns, np.uint64),
+            _arr(v.fn_gather_count, v.n_fns, np.uint32), _arr(v.fn_gather, v.n_gather, np.uint32),
+            _arr(v.fn_tables, v.n_table, np.uint64))
+
+    def expected_lookups(self, fn_steps: int, steps: int) -> int:
+        """Algorithmic table probes: g per step + (A + G) per function-phase step."""
+        a = int(np.count_nonzero(self.grp_alias_size))
+        return self.pert_groups * steps + fn_steps * (a + len(self.grp_offset))
+
+
+class PreparedSimulation:
+    """engine.hpp:22-79 — immutable plan built by :func:`prepare`."""
+
+    def __init__(self, handle, model: Model, theta, k_max, mgp):
+        self._h = C.c_void_p(handle)
+        self.model = model
+        self.theta, self.k_max, self.max_group_parents = theta, k_max, mgp
+        self._view = PlanView()
+        _check(lib.pbn_plan_get_view(self._h, C.byref(self._view)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.pbn_plan_free(self._h)
+            self._h = C.c_void_p(None)
+
+    @property
+    def view(self) -> PlanView:
+        return self._view
+
+    @property
+    def n_kept(self) -> int:
+        return self._view.n_kept
+
+    @property
+    def t(self) -> float:
+        return self._view.t
+
+    def flat(self) -> FlatPlan:
+        return FlatPlan.from_view(self._view)
+
+    def reduced(self):
+        on, nr = C.c_uint32(), C.c_uint32()
+        _check(lib.pbn_plan_reduced(self._h, C.byref(on), C.byref(nr), None, None, None))
+        imap = np.zeros(on.value, np.int32)
+        epos = np.zeros(self.n_kept, np.uint32)
+        rem = np.zeros(max(1, nr.value), np.uint32)
+        _check(lib.pbn_plan_reduced(self._h, None, None, imap.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    _u32p(epos), _u32p(rem)))
+        return {"original_n": on.value, "removed": rem[: nr.value], "index_map": imap,
+                "engine_pos": epos}
+
+    def groups(self):
+        cum = np.zeros(self._view.n_groups + 1, np.uint32)
+        mem = np.zeros(self.n_kept, np.uint32)
+        _check(lib.pbn_plan_groups(self._h, _u32p(mem), _u32p(cum)))
+        return mem, cum
+
+    def compile_predicate(self, terms):
+        """engine.hpp:357-362: [(node, value)] over original indices -> engine bits."""
+        nodes = np.array([t[0] for t in terms], np.uint32)
+        vals = np.array([1 if t[1] else 0 for t in terms], np.uint8)
+        bits = np.zeros(len(terms), np.uint32)
+        _check(lib.pbn_compile_predicate(self._h, _u32p(nodes),
+                                         vals.ctypes.data_as(C.POINTER(C.c_uint8)), len(terms),
+                                         _u32p(bits)))
+        return bits, vals
+
+
+def prepare(model: Model, theta=DEFAULT_THETA, k_max=DEFAULT_K, max_group_parents=DEFAULT_MGP):
+    """engine.hpp:85-164: reduce -> perturbation plan -> partition -> flatten."""
+    h = C.c_void_p()
+    _check(lib.pbn_prepare(model._h, theta, k_max, max_group_parents, C.byref(h)))
+    return PreparedSimulation(h.value, model, theta, k_max, max_group_parents)
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    _check(lib.pbn_device_count(C.byref(c)))
+    return c.value
+
+
+def philox_kat_device(ctrs: np.ndarray, seed: int) -> np.ndarray:
+    """Run Philox4x32-10 on the device for (n,4) uint32 counters (stream known-answer tests)."""
+    ctrs = np.ascontiguousarray(ctrs, dtype=np.uint32)
+    out = np.zeros_like(ctrs)
+    _check(lib.pbn_philox_kat(_u32p(ctrs), ctrs.shape[0], seed, _u32p(out)))
+    return out
+
+
+class GpuEnsemble:
+    """Device-resident plan + ensemble stepping: the drop-in for
+    ``simulate(grouped_simulator, ...)`` (engine.hpp:371-384) over many
+    trajectories, keyed by (seed, global trajectory id, step)."""
+
+    def __init__(self, plan, device: int = 0, lanes_per_traj: int = 0, placement: str = "auto"):
+        view = plan.view if isinstance(plan, PreparedSimulation) else plan
+        self._keep = plan  # the view's arrays must outlive creation
+        self.n_kept = view.n_kept
+        self.words = state_words(self.n_kept)
+        h = C.c_void_p()
+        _check(lib.pbn_gpu_create(C.byref(view), device, lanes_per_traj, C.byref(h)))
+        self._h = h
+        if placement != "auto":
+            self.set_placement(placement)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.pbn_gpu_destroy(self._h)
+            self._h = C.c_void_p(None)
+
+    def set_placement(self, placement: str) -> None:
+        """'auto' | 'global' | 'core' | 'all' (where the plan lives on the device)."""
+        code = {"auto": 0, "global": 1, "core": 2, "all": 3}[placement]
+        _check(lib.pbn_gpu_set_placement(self._h, code))
+
+    def info(self):
+        lpt, place, wpc = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        sm, pb = C.c_uint64(), C.c_uint64()
+        _check(lib.pbn_gpu_info(self._h, C.byref(lpt), C.byref(place), C.byref(sm), C.byref(pb),
+                                C.byref(wpc)))
+        return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "all")[place.value],
+                "staged_smem_bytes": sm.value, "plan_bytes": pb.value,
+                "warps_per_cta": wpc.value}
+
+    def _args(self, seed, traj_begin, n_traj, n_steps, step_begin, pred, stream):
+        a = RunArgs()
+        a.seed, a.traj_begin, a.n_traj = seed, traj_begin, n_traj
+        a.stream, a.step_begin, a.n_steps = stream, step_begin, n_steps
+        if pred is not None and len(pred[0]):
+            bits = np.ascontiguousarray(pred[0], np.uint32)
+            vals = np.ascontiguousarray(pred[1], np.uint8)
+            self._pred_keep = (bits, vals)
+            a.pred_bits = _u32p(bits)
+            a.pred_vals = vals.ctypes.data_as(C.POINTER(C.c_uint8))
+            a.n_pred = len(bits)
+        return a
+
+    def simulate(self, seed, n_traj, n_steps, traj_begin=0, step_begin=0, states=None,
+                 pred=None, stream=STREAM_U53):
+        """HOST buffers in/out. states: (n_traj, words) uint64 engine-order (zeros if None).
+        pred: (engine bits, values) from PreparedSimulation.compile_predicate.
+        Returns (states, counts[n_traj, 8])."""
+        if states is None:
+            states = np.zeros((n_traj, self.words), np.uint64)
+        states = np.ascontiguousarray(states, np.uint64).copy()
+        assert states.shape == (n_traj, self.words)
+        counts = np.zeros((n_traj, COUNT_FIELDS), np.uint64)
+        a = self._args(seed, traj_begin, n_traj, n_steps, step_begin, pred, stream)
+        _check(lib.pbn_gpu_run(self._h, C.byref(a), _u64p(states), _u64p(counts), None))
+        return states, counts
+
+    def simulate_device(self, seed, n_traj, n_steps, d_states, d_counts, traj_begin=0,
+                        step_begin=0, pred=None, stream=STREAM_U53, cuda_stream=0):
+        """DEVICE pointers (ints, e.g. torch tensor .data_ptr()), asynchronous."""
+        a = self._args(seed, traj_begin, n_traj, n_steps, step_begin, pred, stream)
+        _check(lib.pbn_gpu_run_device(self._h, C.byref(a), C.c_void_p(d_states),
+                                      C.c_void_p(d_counts), None, C.c_void_p(cuda_stream)))
+
+    def last_launches(self) -> int:
+        return int(lib.pbn_gpu_last_launches(self._h))

@@ -1,0 +1,474 @@
+// extern "C" boundary of the engine (include/pbn_b200.h). No exception
+// crosses it: reference exception classes map to status codes
+// (errors.hpp:10-32 -> pbn_main.cpp:302-311 exit codes).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pbn_b200.h"
+#include "device/dev_plan.h"
+#include "host/device_plan.hpp"
+#include "host/generator.hpp"
+#include "host/model.hpp"
+#include "host/plan.hpp"
+
+namespace pbn_b200 {
+cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
+                            int stream_kind, std::uint32_t warps_per_cta,
+                            const dev_run_params& rp, std::uint64_t* d_states,
+                            std::uint64_t* d_counts, cudaStream_t stream,
+                            std::uint32_t* launches);
+cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
+                              std::uint32_t n, cudaStream_t stream);
+}  // namespace pbn_b200
+
+using namespace pbn_b200;
+
+struct pbn_model {
+  network net;
+};
+
+struct pbn_plan {
+  prepared_plan pp;
+};
+
+struct cuda_failure : std::runtime_error {
+  explicit cuda_failure(const std::string& w) : std::runtime_error(w) {}
+};
+
+struct pbn_gpu {
+  int device = 0;
+  encoded_plan ep;
+  int place = 0;  // PLACE_* of ensemble.cu
+  std::uint32_t smem_optin = 0, sms = 0;
+  std::uint8_t* d_blob = nullptr;
+  // scratch for the host-buffer entry point
+  std::uint64_t* d_states = nullptr;
+  std::uint64_t* d_counts = nullptr;
+  std::size_t cap_traj = 0;
+  std::uint32_t launches = 0;
+  std::uint32_t last_warps = 0;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return PBN_OK;
+  } catch (const resource_error& e) {
+    g_error = e.what();
+    return PBN_ERESOURCE;
+  } catch (const model_error& e) {
+    g_error = e.what();
+    return PBN_EMODEL;
+  } catch (const cuda_failure& e) {
+    g_error = e.what();
+    return PBN_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_error = "out of host memory";
+    return PBN_ERESOURCE;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return PBN_EUSAGE;
+  }
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw cuda_failure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string("null argument: ") + what);
+}
+
+constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory states
+
+std::uint32_t auto_lpt(std::uint32_t n_kept) {
+  if (n_kept <= 96) return 4;
+  if (n_kept <= 256) return 8;
+  if (n_kept <= 512) return 16;
+  return 32;
+}
+
+std::uint32_t staged_bytes(const pbn_gpu& g) {
+  if (g.place == 2) return g.ep.h.core_bytes + g.ep.h.table_bytes;
+  if (g.place == 1) return g.ep.h.core_bytes;
+  return 0;
+}
+
+// Warps per CTA: enough resident slots for the whole ensemble in one wave
+// (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
+std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj) {
+  const std::uint32_t lpt = g.ep.h.lpt;
+  const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
+  std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
+  w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(32, w));
+  const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * 2 * g.ep.h.sw32 * 4;
+  const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
+  while (w > 1 && w * per_warp > avail) --w;
+  if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
+  return static_cast<std::uint32_t>(w);
+}
+
+dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
+  dev_run_params rp{};
+  philox_round_keys(a.seed, rp.rk0, rp.rk1);
+  rp.traj_begin = a.traj_begin;
+  rp.n_traj = a.n_traj;
+  rp.step_begin = a.step_begin;
+  rp.n_steps = a.n_steps;
+  if (a.n_pred) {
+    need(a.pred_bits, "pred_bits");
+    need(a.pred_vals, "pred_vals");
+  }
+  rp.pred = compile_dev_predicate(a.pred_bits, a.pred_vals, a.n_pred, g.ep.h.n_kept);
+  if (a.stream != PBN_STREAM_U53 && a.stream != PBN_STREAM_U32)
+    throw std::invalid_argument("unknown stream kind");
+  if (a.stream == PBN_STREAM_U32 && !g.ep.h.u32_ok)
+    throw resource_error("U32 stream needs every group alias table <= 2^21 cells");
+  if (a.flags & PBN_RUN_NODE_COUNTS)
+    throw std::invalid_argument("per-node counts are not implemented on the device yet");
+  if (a.traj_begin + a.n_traj > (1ull << 32))
+    throw std::invalid_argument("trajectory ids must fit in 32 bits");
+  return rp;
+}
+
+void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
+                std::uint64_t* d_counts, cudaStream_t stream) {
+  const dev_run_params rp = make_params(g, a);
+  if (a.n_traj == 0) return;
+  ck(cudaSetDevice(g.device), "cudaSetDevice");
+  g.last_warps = pick_warps(g, a.n_traj);
+  g.launches = 0;
+  ck(launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_warps, rp,
+                     d_states, d_counts, stream, &g.launches),
+     "ensemble launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pbn_last_error(void) { return g_error.c_str(); }
+const char* pbn_version(void) { return "pbn_b200 0.1 (sm_100a)"; }
+uint32_t pbn_state_words(uint32_t n_kept) { return n_kept / 64 + 1; }
+
+int pbn_model_parse(const char* text, size_t len, pbn_model** out) {
+  return guard([&] {
+    need(text, "text");
+    need(out, "out");
+    auto m = std::make_unique<pbn_model>();
+    m->net = parse_network(std::string(text, len));
+    *out = m.release();
+  });
+}
+
+int pbn_model_serialize(const pbn_model* m, char* buf, size_t cap, size_t* len_out) {
+  return guard([&] {
+    need(m, "model");
+    const std::string s = serialize_network(m->net);
+    if (len_out) *len_out = s.size();
+    if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+  });
+}
+
+int pbn_model_generate(const pbn_gen_params* gp, pbn_model** out, uint32_t* pred_nodes,
+                       uint8_t* pred_vals, uint32_t* n_pred_out) {
+  return guard([&] {
+    need(gp, "params");
+    need(out, "out");
+    gen_params p;
+    p.n = gp->n;
+    p.f_min = gp->f_min;
+    p.f_max = gp->f_max;
+    p.p_min = gp->p_min;
+    p.p_max = gp->p_max;
+    p.leaf_frac = gp->leaf_frac;
+    p.p = gp->perturbation;
+    p.n_targets = gp->n_targets;
+    p.targets_fixed = gp->targets_fixed != 0;
+    p.seed = gp->seed;
+    generated_network g = generate_network(p);
+    if (pred_nodes)
+      std::copy(g.pred_nodes.begin(), g.pred_nodes.end(), pred_nodes);
+    if (pred_vals) std::copy(g.pred_vals.begin(), g.pred_vals.end(), pred_vals);
+    if (n_pred_out) *n_pred_out = static_cast<uint32_t>(g.pred_nodes.size());
+    auto m = std::make_unique<pbn_model>();
+    m->net = std::move(g.net);
+    *out = m.release();
+  });
+}
+
+int pbn_model_info(const pbn_model* m, uint32_t* n, double* p, uint32_t* n_interest,
+                   double* density) {
+  return guard([&] {
+    need(m, "model");
+    if (n) *n = m->net.size();
+    if (p) *p = m->net.p;
+    if (n_interest) *n_interest = static_cast<uint32_t>(m->net.interest.size());
+    if (density) *density = network_density(m->net);
+  });
+}
+
+int pbn_model_node_index(const pbn_model* m, const char* name, uint32_t* index_out) {
+  return guard([&] {
+    need(m, "model");
+    need(name, "name");
+    for (uint32_t i = 0; i < m->net.size(); ++i)
+      if (m->net.nodes[i].name == name) {
+        *index_out = i;
+        return;
+      }
+    throw model_error(std::string("unknown node '") + name + "'");
+  });
+}
+
+void pbn_model_free(pbn_model* m) { delete m; }
+
+int pbn_prepare(const pbn_model* m, uint64_t theta, uint32_t k_max, uint32_t mgp,
+                pbn_plan** out) {
+  return guard([&] {
+    need(m, "model");
+    need(out, "out");
+    auto p = std::make_unique<pbn_plan>();
+    p->pp = prepare_plan(m->net, theta, k_max, mgp);
+    *out = p.release();
+  });
+}
+
+int pbn_plan_get_view(const pbn_plan* plan, pbn_plan_view* v) {
+  return guard([&] {
+    need(plan, "plan");
+    need(v, "view");
+    const prepared_plan& pp = plan->pp;
+    std::memset(v, 0, sizeof *v);
+    v->n_kept = pp.n_kept();
+    v->t = pp.t;
+    v->pert_groups = pp.g;
+    v->pert_k = pp.k;
+    v->pert_k_prime = pp.k_prime;
+    v->pert_size = pp.pert.size();
+    v->pert_mask = pp.mask;
+    v->pert_cut = pp.pert.cut.data();
+    v->pert_alias = pp.pert.alias.data();
+    v->n_groups = static_cast<uint32_t>(pp.grp_offset.size());
+    v->grp_offset = pp.grp_offset.data();
+    v->grp_fn_begin = pp.grp_fn_begin.data();
+    v->grp_alias_begin = pp.grp_alias_begin.data();
+    v->grp_alias_size = pp.grp_alias_size.data();
+    v->n_alias = pp.alias_cut.size();
+    v->alias_cut = pp.alias_cut.data();
+    v->alias_idx = pp.alias_idx.data();
+    v->n_fns = static_cast<uint32_t>(pp.fn_gather_begin.size());
+    v->fn_gather_begin = pp.fn_gather_begin.data();
+    v->fn_table_begin = pp.fn_table_begin.data();
+    v->fn_gather_count = pp.fn_gather_count.data();
+    v->n_gather = pp.fn_gather.size();
+    v->fn_gather = pp.fn_gather.data();
+    v->n_table = pp.fn_tables.size();
+    v->fn_tables = pp.fn_tables.data();
+  });
+}
+
+int pbn_plan_reduced(const pbn_plan* plan, uint32_t* original_n, uint32_t* n_removed,
+                     int32_t* index_map, uint32_t* engine_pos, uint32_t* removed) {
+  return guard([&] {
+    need(plan, "plan");
+    const prepared_plan& pp = plan->pp;
+    if (original_n) *original_n = pp.original_n;
+    if (n_removed) *n_removed = static_cast<uint32_t>(pp.removed.size());
+    if (index_map) std::copy(pp.index_map.begin(), pp.index_map.end(), index_map);
+    if (engine_pos) std::copy(pp.engine_pos.begin(), pp.engine_pos.end(), engine_pos);
+    if (removed) std::copy(pp.removed.begin(), pp.removed.end(), removed);
+  });
+}
+
+int pbn_plan_groups(const pbn_plan* plan, uint32_t* members, uint32_t* cum) {
+  return guard([&] {
+    need(plan, "plan");
+    const prepared_plan& pp = plan->pp;
+    std::size_t k = 0;
+    if (members)
+      for (const auto& g : pp.members)
+        for (auto v : g) members[k++] = v;
+    if (cum) std::copy(pp.cum.begin(), pp.cum.end(), cum);
+  });
+}
+
+int pbn_compile_predicate(const pbn_plan* plan, const uint32_t* nodes, const uint8_t* vals,
+                          uint32_t n, uint32_t* bits) {
+  return guard([&] {
+    need(plan, "plan");
+    const prepared_plan& pp = plan->pp;
+    for (uint32_t i = 0; i < n; ++i) {  // engine.hpp:343-362
+      if (nodes[i] >= pp.original_n) throw model_error("predicate references a nonexistent node");
+      const int32_t r = pp.index_map[nodes[i]];
+      if (r < 0) throw model_error("predicate references a removed leaf node");
+      bits[i] = pp.engine_pos[static_cast<uint32_t>(r)];
+    }
+    (void)vals;
+  });
+}
+
+void pbn_plan_free(pbn_plan* plan) { delete plan; }
+
+int pbn_device_count(int* count) {
+  return guard([&] {
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu** out) {
+  return guard([&] {
+    need(view, "view");
+    need(out, "out");
+    auto g = std::make_unique<pbn_gpu>();
+    g->device = device;
+    g->ep = encode_plan(*view, lpt ? lpt : auto_lpt(view->n_kept));
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    int optin = 0, sms = 0;
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    g->smem_optin = static_cast<uint32_t>(optin);
+    g->sms = static_cast<uint32_t>(sms);
+    const dev_plan_header& h = g->ep.h;
+    if (h.core_bytes + h.table_bytes + kStateReserve <= g->smem_optin)
+      g->place = 2;
+    else if (h.core_bytes + kStateReserve <= g->smem_optin)
+      g->place = 1;
+    else
+      g->place = 0;
+    ck(cudaMalloc(&g->d_blob, g->ep.blob.size()), "cudaMalloc plan");
+    ck(cudaMemcpy(g->d_blob, g->ep.blob.data(), g->ep.blob.size(), cudaMemcpyHostToDevice),
+       "upload plan");
+    *out = g.release();
+  });
+}
+
+int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement) {
+  return guard([&] {
+    need(g, "gpu");
+    if (placement > 3) throw std::invalid_argument("placement must be 0..3");
+    if (placement == 0) return;
+    const int want = static_cast<int>(placement) - 1;  // 0 global, 1 core, 2 all
+    const dev_plan_header& h = g->ep.h;
+    const std::uint64_t need_bytes = want == 2 ? h.core_bytes + h.table_bytes
+                                     : want == 1 ? h.core_bytes
+                                                 : 0;
+    if (need_bytes + 4096 > g->smem_optin)
+      throw resource_error("requested placement does not fit in shared memory");
+    g->place = want;
+  });
+}
+
+int pbn_gpu_info(const pbn_gpu* g, uint32_t* lpt, uint32_t* tables_in_smem, uint64_t* smem_bytes,
+                 uint64_t* plan_bytes, uint32_t* warps_per_cta) {
+  return guard([&] {
+    need(g, "gpu");
+    if (lpt) *lpt = g->ep.h.lpt;
+    if (tables_in_smem) *tables_in_smem = static_cast<uint32_t>(g->place);
+    if (smem_bytes) *smem_bytes = staged_bytes(*g);
+    if (plan_bytes) *plan_bytes = g->ep.blob.size();
+    if (warps_per_cta) *warps_per_cta = g->last_warps;
+  });
+}
+
+int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* counts,
+                uint64_t* node_counts) {
+  return guard([&] {
+    need(g, "gpu");
+    need(a, "args");
+    need(states, "states");
+    need(counts, "counts");
+    (void)node_counts;
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    const std::size_t words = pbn_state_words(g->ep.h.n_kept);
+    if (a->n_traj > g->cap_traj) {
+      if (g->d_states) cudaFree(g->d_states);
+      if (g->d_counts) cudaFree(g->d_counts);
+      g->d_states = g->d_counts = nullptr;
+      g->cap_traj = 0;
+      ck(cudaMalloc(&g->d_states, 8 * words * a->n_traj), "cudaMalloc states");
+      ck(cudaMalloc(&g->d_counts, 8 * PBN_COUNT_FIELDS * static_cast<std::size_t>(a->n_traj)),
+         "cudaMalloc counts");
+      g->cap_traj = a->n_traj;
+    }
+    if (a->n_traj == 0) return;
+    ck(cudaMemcpy(g->d_states, states, 8 * words * a->n_traj, cudaMemcpyHostToDevice), "H2D");
+    run_device(*g, *a, g->d_states, g->d_counts, nullptr);
+    ck(cudaMemcpy(states, g->d_states, 8 * words * a->n_traj, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(counts, g->d_counts, 8 * PBN_COUNT_FIELDS * static_cast<std::size_t>(a->n_traj),
+                  cudaMemcpyDeviceToHost),
+       "D2H");
+  });
+}
+
+int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states, uint64_t* d_counts,
+                       uint64_t* d_node_counts, void* stream) {
+  return guard([&] {
+    need(g, "gpu");
+    need(a, "args");
+    (void)d_node_counts;
+    run_device(*g, *a, d_states, d_counts, static_cast<cudaStream_t>(stream));
+  });
+}
+
+uint32_t pbn_gpu_last_launches(const pbn_gpu* g) { return g ? g->launches : 0; }
+
+void pbn_gpu_destroy(pbn_gpu* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->d_blob) cudaFree(g->d_blob);
+  if (g->d_states) cudaFree(g->d_states);
+  if (g->d_counts) cudaFree(g->d_counts);
+  delete g;
+}
+
+// Known-answer hook for the stream (tests): n counters (4 u32 each) -> blocks.
+int pbn_philox_kat(const uint32_t* ctr, uint32_t n, uint64_t seed, uint32_t* out) {
+  return guard([&] {
+    uint4 *d_in = nullptr, *d_out = nullptr;
+    ck(cudaMalloc(&d_in, 16 * static_cast<std::size_t>(n)), "malloc");
+    ck(cudaMalloc(&d_out, 16 * static_cast<std::size_t>(n)), "malloc");
+    ck(cudaMemcpy(d_in, ctr, 16 * static_cast<std::size_t>(n), cudaMemcpyHostToDevice), "H2D");
+    ck(launch_philox_kat(d_in, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32),
+                         d_out, n, nullptr),
+       "kat");
+    ck(cudaMemcpy(out, d_out, 16 * static_cast<std::size_t>(n), cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d_in);
+    cudaFree(d_out);
+  });
+}
+
+int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pred_bits,
+                 const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
+                 pbn_estimate_result* out) {
+  return guard([&] {
+    need(g, "gpu");
+    need(req, "request");
+    need(out, "result");
+    (void)pred_bits;
+    (void)pred_vals;
+    (void)n_pred;
+    (void)states_inout;
+    throw std::invalid_argument("pbn_estimate: not implemented yet");
+  });
+}
+
+}  // extern "C"

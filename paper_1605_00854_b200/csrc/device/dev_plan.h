@@ -1,0 +1,72 @@
+// Device encoding of a prepared plan: one contiguous, 16-byte-aligned blob the
+// kernel stages into shared memory with a 1-D bulk copy (cp.async.bulk), plus
+// a small header passed by value as a kernel parameter.
+//
+// Layout (all offsets in bytes from the blob start, each section 16-aligned):
+//   pert53[2^k]   u64  perturbation cells for the U53 stream:
+//                      bits [0, 53-k) threshold T, bits [53-k, 53) cell result
+//                      on a miss. A draw r53 picks cell c = r53 >> (53-k) and
+//                      returns (r53 & (2^(53-k)-1)) < T ? c : alias — exactly
+//                      alias_table::next (alias.hpp:70-76) for N = 2^k, where
+//                      T = ceil(cut * 2^(53-k)); cells whose cut rounds to the
+//                      whole range store (T=0, alias=c).
+//   pert32[2^k]   u32  the same for the U32 stream with 32-k threshold bits.
+//   groups[G]     uint4 {offset, fn_begin, alias_begin, alias_size | (members-1)<<24}
+//   fns[F]        uint2 {table byte offset, (gather record start << 5) | gather count}
+//   grec[...]     u16  gather records, 4-aligned per function, padded with the
+//                      always-zero bit n' (engine.hpp:149-150):
+//                      (word32 << 5) | ((bit32 - slot) & 31) — a funnel rotate
+//                      by the low 5 bits lands the parent bit at `slot`.
+//   acut[A]       f64  group alias cut-offs (U53 path, FP64 like engine.hpp:285-290)
+//   aidx[A]       u32  group alias targets
+//   a32[A]        uint2 {ceil(cut * 2^32) or 0, alias or self}: U32 integer path
+//   buckets[L+1]  u32  group range of lane r: [buckets[r], buckets[r+1])
+//   aord[L]       u32  alias ordinal of the first alias group in lane r's range
+//   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
+#pragma once
+
+#include <cstdint>
+
+namespace pbn_b200 {
+
+inline constexpr std::uint32_t kMaxPredWords = 16;
+
+struct dev_plan_header {
+  std::uint32_t n_kept;
+  std::uint32_t sw32;       // u32 state words per trajectory (= 2 * (n_kept/64 + 1))
+  std::uint32_t g;          // perturbation groups
+  std::uint32_t k;          // perturbation width
+  std::uint32_t last_mask;  // 2^k' - 1 (k' <= 24)
+  std::uint32_t n_groups;
+  std::uint32_t lpt;        // lanes per trajectory the buckets were cut for
+  std::uint32_t max_alias;  // largest group alias table
+  std::uint64_t leaf_thr53; // floor(t * 2^53): leaf perturbation iff r53 > thr
+  std::uint32_t leaf_thr32; // floor(t * 2^32) (saturated)
+  std::uint32_t leaf_never; // t == 1: the leaf draw can never fire
+  std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
+  std::uint32_t off_acut, off_aidx, off_a32, off_buckets, off_aord, off_tables;
+  std::uint32_t core_bytes;   // bytes [0, off_tables)
+  std::uint32_t table_bytes;  // bytes [off_tables, off_tables + table_bytes)
+  std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
+};
+
+// Compiled predicate: the state satisfies it iff for every i,
+// (word[w[i]] & mask[i]) == want[i].
+struct dev_predicate {
+  std::uint32_t n;
+  std::uint32_t w[kMaxPredWords];
+  std::uint32_t mask[kMaxPredWords];
+  std::uint32_t want[kMaxPredWords];
+};
+
+struct dev_run_params {
+  std::uint32_t rk0[10], rk1[10];  // Philox round keys of the seed
+  std::uint64_t traj_begin;
+  std::uint32_t n_traj;
+  std::uint32_t pad0;
+  std::uint64_t step_begin;
+  std::uint64_t n_steps;
+  dev_predicate pred;
+};
+
+}  // namespace pbn_b200

@@ -1,0 +1,427 @@
+// Ensemble trajectory kernel: many independent PBN trajectories, each advanced
+// `n_steps` steps of the structure-based stepper (Alg. 5 of the paper; the
+// reference's grouped_simulator::step, engine.hpp:255-312, driven by
+// simulate(), engine.hpp:371-384), bit-exact on the injected Philox stream.
+//
+// Work decomposition: one trajectory per sub-warp of LPT lanes (LPT = 32:
+// one per warp; LPT = 1: one per thread). Lane r of a sub-warp
+//   * draws Philox blocks r, r+LPT, ... of the step's first g+1 draws (the g
+//     grouped-perturbation draws and the leaf draw) and XORs any flip into the
+//     state (engine.hpp:257-266);
+//   * a sub-warp ballot implements the short-circuit: any kept flip ends the
+//     step (engine.hpp:267); otherwise the leaf draw decides (engine.hpp:268);
+//   * in the function phase lane r owns a contiguous range of node groups
+//     (host-balanced buckets): per group one alias draw (engine.hpp:284-291),
+//     a gather of the chosen combined function's parent bits from the shared
+//     state (engine.hpp:292-302), one table lookup (engine.hpp:303) and an OR
+//     into the next state (engine.hpp:304-309), accumulated in a 96-bit
+//     register window and flushed with shared-memory atomics at word changes.
+// The plan (perturbation cells, group/function records, gather records,
+// alias cells and — when they fit — the truth tables) is staged once per CTA
+// into shared memory with one bulk copy (cp.async.bulk + mbarrier). States
+// live in shared memory (two buffers per trajectory). Statistics stay in
+// registers and are written once at the end.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dev_plan.h"
+#include "philox.cuh"
+
+namespace pbn_b200 {
+
+enum { STREAM_U53 = 0, STREAM_U32 = 1 };
+// Plan placement: 2 = whole blob in smem, 1 = core in smem + tables in global,
+// 0 = everything in global (read through the read-only L1/L2 path).
+enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_ALL = 2 };
+
+template <bool G, class T>
+__device__ __forceinline__ T ldp(const T* p) {
+  if constexpr (G)
+    return __ldg(p);
+  else
+    return *p;
+}
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Stage `bytes` (multiple of 16) from global to shared memory with bulk
+// copies completing on one mbarrier; every thread of the CTA waits.
+__device__ __forceinline__ void stage_plan(std::uint8_t* dst, const std::uint8_t* src,
+                                           std::uint32_t bytes, std::uint64_t* bar) {
+  const std::uint32_t b = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+    for (std::uint32_t off = 0; off < bytes; off += 32768u) {
+      const std::uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(dst + off)),
+          "l"(src + off), "r"(n), "r"(b)
+          : "memory");
+    }
+  }
+  __syncthreads();
+  std::uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(b)
+        : "memory");
+  }
+}
+
+template <int STREAM>
+struct draws {
+  static constexpr std::uint32_t kPerBlock = STREAM == STREAM_U53 ? 2 : 4;
+};
+
+// Raw draw e of a Philox block: r53 as (hi32, lo21) pieces for U53, r32 for U32.
+struct raw53 {
+  std::uint32_t hi;  // bits [21, 53) of r53  (= x[2e+1])
+  std::uint32_t lo;  // x[2e]; bits [0, 21) of r53 are lo >> 11
+  __device__ __forceinline__ std::uint64_t value() const {
+    return (static_cast<std::uint64_t>(hi) << 21) | (lo >> 11);
+  }
+};
+
+__device__ __forceinline__ raw53 pick53(const uint4& x, std::uint32_t e) {
+  return e == 0 ? raw53{x.y, x.x} : raw53{x.w, x.z};
+}
+__device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e) {
+  return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
+}
+
+// Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form.
+template <bool G>
+__device__ __forceinline__ std::uint32_t pert_draw53(const std::uint64_t* cells, raw53 r,
+                                                     std::uint32_t k) {
+  const std::uint32_t c = r.hi >> (32 - k);
+  const std::uint32_t lbits = 53 - k;
+  const std::uint64_t lmask = (1ull << lbits) - 1;
+  const std::uint64_t low = r.value() & lmask;
+  const std::uint64_t e = ldp<G>(cells + c);
+  return low < (e & lmask) ? c : static_cast<std::uint32_t>(e >> lbits);
+}
+
+template <bool G>
+__device__ __forceinline__ std::uint32_t pert_draw32(const std::uint32_t* cells, std::uint32_t r,
+                                                     std::uint32_t k) {
+  const std::uint32_t c = r >> (32 - k);
+  const std::uint32_t lmask = (1u << (32 - k)) - 1;
+  const std::uint32_t e = ldp<G>(cells + c);
+  return (r & lmask) < (e & lmask) ? c : (e >> (32 - k));
+}
+
+template <int LPT, int STREAM, int PLACE>
+__global__ void __launch_bounds__(1024, 1)
+    pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
+                        const dev_run_params rp, std::uint64_t* __restrict__ states,
+                        std::uint64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) std::uint8_t smem[];
+  __shared__ std::uint64_t stage_bar;
+  constexpr bool GC = PLACE == PLACE_GLOBAL;  // core sections read from global
+  constexpr bool GT = PLACE != PLACE_ALL;     // tables read from global
+  constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
+
+  std::uint32_t staged = 0;
+  if constexpr (PLACE == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
+  if constexpr (PLACE == PLACE_CORE) staged = h.core_bytes;
+  if (staged) stage_plan(smem, gblob, staged, &stage_bar);
+
+  const std::uint8_t* core = GC ? gblob : smem;
+  const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
+  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(core + h.off_pert53);
+  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(core + h.off_pert32);
+  const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
+  const uint2* fns = reinterpret_cast<const uint2*>(core + h.off_fns);
+  const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
+  const double* acut = reinterpret_cast<const double*>(core + h.off_acut);
+  const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(core + h.off_aidx);
+  const uint2* a32 = reinterpret_cast<const uint2*>(core + h.off_a32);
+  const std::uint32_t* buckets = reinterpret_cast<const std::uint32_t*>(core + h.off_buckets);
+  const std::uint32_t* aord = reinterpret_cast<const std::uint32_t*>(core + h.off_aord);
+  const std::uint32_t* tab32 = reinterpret_cast<const std::uint32_t*>(tab);
+  const std::uint64_t* tab64 = reinterpret_cast<const std::uint64_t*>(tab);
+
+  const std::uint32_t lane = threadIdx.x & 31;
+  const std::uint32_t r = lane % LPT;
+  const std::uint32_t sub = lane / LPT;
+  const std::uint32_t smask =
+      LPT == 32 ? 0xFFFFFFFFu : (((1u << (LPT & 31)) - 1u) << ((sub * LPT) & 31));
+  const std::uint32_t slots = blockDim.x / LPT;
+  const std::uint32_t slot = threadIdx.x / LPT;
+  const std::uint64_t tloc = static_cast<std::uint64_t>(blockIdx.x) * slots + slot;
+  if (tloc >= rp.n_traj) return;
+
+  const std::uint32_t sw32 = h.sw32;
+  std::uint32_t* st_area = reinterpret_cast<std::uint32_t*>(smem + staged);
+  std::uint32_t* S0 = st_area + static_cast<std::size_t>(slot) * 2 * sw32;
+  std::uint32_t* S1 = S0 + sw32;
+  {
+    const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
+    for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w];
+  }
+  __syncwarp(smask);
+
+  const std::uint32_t k = h.k, g = h.g;
+  const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks holding draws 0..g
+  const std::uint32_t gb0 = ldp<GC>(buckets + r), gb1 = ldp<GC>(buckets + r + 1);
+  const std::uint32_t ord0 = ldp<GC>(aord + r);
+  const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
+  std::uint32_t thi0, tlo0;
+  mulhilo(kPhiloxM0, traj, thi0, tlo0);
+
+  auto pred_eval = [&](const std::uint32_t* S) -> std::uint32_t {
+    std::uint32_t ok = rp.pred.n ? 1u : 0u;
+    for (std::uint32_t i = 0; i < rp.pred.n; ++i)
+      ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
+    return ok;
+  };
+
+  std::uint32_t cur = 0;
+  std::uint32_t prev = pred_eval(S0);
+  std::uint32_t n01 = 0, n10 = 0, n11 = 0, nfn = 0, npert = 0;
+  const std::uint64_t s_end = rp.step_begin + rp.n_steps;
+
+  for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
+    std::uint32_t* Sc = cur ? S1 : S0;
+    const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+
+    // ---- grouped perturbation + leaf draw (draws 0..g)
+    bool flip = false, leaf = false;
+    for (std::uint32_t b = r; b < nb0; b += LPT) {
+      const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+#pragma unroll
+      for (std::uint32_t e = 0; e < DPB; ++e) {
+        const std::uint32_t d = b * DPB + e;
+        if (d < g) {
+          std::uint32_t c;
+          if constexpr (STREAM == STREAM_U53)
+            c = pert_draw53<GC>(pert53, pick53(x, e), k);
+          else
+            c = pert_draw32<GC>(pert32, pick32(x, e), k);
+          if (d + 1 == g) c &= h.last_mask;
+          if (c != 0) {  // xor_chunk (bitstate.hpp:50-58); rare
+            flip = true;
+            const std::uint32_t o = d * k, w = o >> 5, sh = o & 31;
+            atomicXor(Sc + w, c << sh);
+            if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
+          }
+        } else if (d == g) {
+          if constexpr (STREAM == STREAM_U53)
+            leaf = pick53(x, e).value() > h.leaf_thr53;
+          else
+            leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
+        }
+      }
+    }
+    const bool any_flip = __ballot_sync(smask, flip) != 0;
+    const bool any_leaf = __ballot_sync(smask, leaf) != 0;
+
+    if (any_flip) {
+      __syncwarp(smask);
+      ++npert;
+    } else if (!any_leaf) {
+      // ---- function phase
+      std::uint32_t* Sn = cur ? S0 : S1;
+      for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
+      __syncwarp(smask);
+      std::uint32_t a0 = 0, a1 = 0, a2 = 0;
+      std::uint32_t cw = gb0 < gb1 ? (ldp<GC>(groups + gb0).x >> 5) : 0;
+      std::uint32_t ord = ord0;
+      std::uint32_t bcached = 0xFFFFFFFFu;
+      uint4 bx = make_uint4(0, 0, 0, 0);
+      for (std::uint32_t gi = gb0; gi < gb1; ++gi) {
+        const uint4 G = ldp<GC>(groups + gi);
+        const std::uint32_t asz = G.w & 0x7FFFFFu;
+        const std::uint32_t members = (G.w >> 24) + 1;
+        std::uint32_t idx = 0;
+        if (asz != 0) {
+          const std::uint32_t d = g + 1 + ord;
+          ++ord;
+          const std::uint32_t blk = d / DPB, e = d % DPB;
+          if (blk != bcached) {
+            bx = philox_block(sp, blk, rp.rk0, rp.rk1);
+            bcached = blk;
+          }
+          if constexpr (STREAM == STREAM_U53) {
+            // u*N, truncation, clamp, fraction vs cut-off — in IEEE double
+            // without contraction, as engine.hpp:285-290 computes it.
+            const double u = __ull2double_rn(pick53(bx, e).value()) * 0x1.0p-53;
+            const double xx = __dmul_rn(u, __uint2double_rn(asz));
+            std::uint32_t c = __double2uint_rz(xx);
+            if (c >= asz) c = asz - 1;
+            const double fr = __dsub_rn(xx, __uint2double_rn(c));
+            idx = fr < ldp<GC>(acut + G.z + c) ? c : ldp<GC>(aidx + G.z + c);
+          } else {
+            const std::uint64_t P = static_cast<std::uint64_t>(pick32(bx, e)) * asz;
+            const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
+            const uint2 cell = ldp<GC>(a32 + G.z + c);
+            idx = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
+          }
+        }
+        const uint2 F = ldp<GC>(fns + G.y + idx);
+        const std::uint32_t gc = F.y & 31u;
+        const std::uint32_t rb = F.y >> 7;  // record quad index (records are 4-aligned)
+        std::uint32_t v = 0;
+        for (std::uint32_t j = 0; j < gc; j += 4) {
+          const uint2 q = ldp<GC>(grec + rb + (j >> 2));
+          const std::uint32_t r0 = q.x & 0xFFFFu, r1 = q.x >> 16, r2 = q.y & 0xFFFFu,
+                              r3 = q.y >> 16;
+          const std::uint32_t w0 = Sc[r0 >> 5], w1 = Sc[r1 >> 5], w2 = Sc[r2 >> 5],
+                              w3 = Sc[r3 >> 5];
+          v |= (__funnelshift_r(w0, w0, r0) & (1u << j)) |
+               (__funnelshift_r(w1, w1, r1) & (2u << j)) |
+               (__funnelshift_r(w2, w2, r2) & (4u << j)) |
+               (__funnelshift_r(w3, w3, r3) & (8u << j));
+        }
+        // table lookup (engine.hpp:303), entries of 1/2/4/8 bytes
+        std::uint32_t olo, ohi = 0;
+        if (members <= 32) {
+          const std::uint32_t el2 = members <= 8 ? 0 : members <= 16 ? 1 : 2;
+          const std::uint32_t addr = F.x + (v << el2);
+          const std::uint32_t word = ldp<GT>(tab32 + (addr >> 2));
+          const std::uint32_t m = members == 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
+          olo = (word >> ((addr & 3u) << 3)) & m;
+        } else {
+          const std::uint64_t o64 = ldp<GT>(tab64 + (F.x >> 3) + v);
+          olo = static_cast<std::uint32_t>(o64);
+          ohi = static_cast<std::uint32_t>(o64 >> 32);
+        }
+        // OR into the next state at the group offset (engine.hpp:304-309)
+        const std::uint32_t w = G.x >> 5, sh = G.x & 31;
+        while (cw < w) {
+          if (a0) atomicOr(Sn + cw, a0);
+          a0 = a1;
+          a1 = a2;
+          a2 = 0;
+          ++cw;
+        }
+        a0 |= olo << sh;
+        a1 |= sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
+        a2 |= sh ? (ohi >> (32 - sh)) : 0u;
+      }
+      if (a0) atomicOr(Sn + cw, a0);
+      if (a1) atomicOr(Sn + cw + 1, a1);
+      if (a2) atomicOr(Sn + cw + 2, a2);
+      __syncwarp(smask);
+      cur ^= 1;
+      ++nfn;
+    }
+
+    // ---- statistics (engine.hpp:375-381) + predicate transitions
+    const std::uint32_t hit = pred_eval(cur ? S1 : S0);
+    n01 += (prev == 0) & (hit == 1);
+    n10 += (prev == 1) & (hit == 0);
+    n11 += (prev == 1) & (hit == 1);
+    prev = hit;
+    __syncwarp(smask);
+  }
+
+  {
+    const std::uint32_t* Sf = cur ? S1 : S0;
+    std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(states + tloc * (sw32 / 2));
+    for (std::uint32_t w = r; w < sw32; w += LPT) dst[w] = Sf[w];
+  }
+  if (r == 0) {
+    std::uint64_t* c = counts + tloc * 8;
+    const std::uint64_t steps = rp.n_steps;
+    const std::uint64_t t11 = n11, t01 = n01, t10 = n10;
+    c[0] = steps;
+    c[1] = rp.pred.n ? t01 + t11 : 0;
+    c[2] = rp.pred.n ? steps - t01 - t10 - t11 : 0;
+    c[3] = rp.pred.n ? t01 : 0;
+    c[4] = rp.pred.n ? t10 : 0;
+    c[5] = rp.pred.n ? t11 : 0;
+    c[6] = nfn;
+    c[7] = npert;
+  }
+}
+
+// Known-answer kernel for the stream: out[i] = Philox4x32-10(ctr[i], key).
+__global__ void pbn_philox_kat_kernel(const uint4* ctr, std::uint32_t k0, std::uint32_t k1,
+                                      uint4* out, std::uint32_t n) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox4x32_10(ctr[i], k0, k1);
+}
+
+// ----------------------------------------------------------------------------
+// Host-side launch helpers (called from capi.cpp).
+
+using kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
+                           std::uint64_t*, std::uint64_t*);
+
+template <int LPT, int STREAM>
+kernel_fn pick_place(int place) {
+  switch (place) {
+    case PLACE_ALL:
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL>;
+    case PLACE_CORE:
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE>;
+    default:
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL>;
+  }
+}
+
+template <int STREAM>
+kernel_fn pick_lpt(std::uint32_t lpt, int place) {
+  switch (lpt) {
+    case 1:
+      return pick_place<1, STREAM>(place);
+    case 2:
+      return pick_place<2, STREAM>(place);
+    case 4:
+      return pick_place<4, STREAM>(place);
+    case 8:
+      return pick_place<8, STREAM>(place);
+    case 16:
+      return pick_place<16, STREAM>(place);
+    default:
+      return pick_place<32, STREAM>(place);
+  }
+}
+
+kernel_fn select_kernel(std::uint32_t lpt, int stream, int place) {
+  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place)
+                              : pick_lpt<STREAM_U32>(lpt, place);
+}
+
+cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
+                            int stream_kind, std::uint32_t warps_per_cta,
+                            const dev_run_params& rp, std::uint64_t* d_states,
+                            std::uint64_t* d_counts, cudaStream_t stream,
+                            std::uint32_t* launches) {
+  const kernel_fn fn = select_kernel(h.lpt, stream_kind, place);
+  const std::uint32_t threads = warps_per_cta * 32;
+  const std::uint32_t slots = threads / h.lpt;
+  const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;
+  std::size_t staged = 0;
+  if (place == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
+  if (place == PLACE_CORE) staged = h.core_bytes;
+  const std::size_t smem = staged + static_cast<std::size_t>(slots) * 2 * h.sw32 * 4;
+  cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  if (grid == 0) return cudaSuccess;
+  fn<<<grid, threads, smem, stream>>>(h, d_blob, rp, d_states, d_counts);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
+                              std::uint32_t n, cudaStream_t stream) {
+  pbn_philox_kat_kernel<<<(n + 127) / 128, 128, 0, stream>>>(d_ctr, k0, k1, d_out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace pbn_b200

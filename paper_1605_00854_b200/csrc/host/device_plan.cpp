@@ -1,0 +1,266 @@
+// Device plan encoder; see device_plan.hpp and dev_plan.h for the layout.
+#include "device_plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "model.hpp"
+
+namespace pbn_b200 {
+
+namespace {
+
+std::uint32_t entry_log2(std::uint32_t members) {
+  return members <= 8 ? 0 : members <= 16 ? 1 : members <= 32 ? 2 : 3;
+}
+
+std::size_t align16(std::size_t x) { return (x + 15) & ~std::size_t(15); }
+
+template <class T>
+void put(std::vector<std::uint8_t>& blob, std::size_t off, const std::vector<T>& v) {
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), sizeof(T) * v.size());
+}
+
+}  // namespace
+
+void philox_round_keys(std::uint64_t seed, std::uint32_t rk0[10], std::uint32_t rk1[10]) {
+  std::uint32_t k0 = static_cast<std::uint32_t>(seed), k1 = static_cast<std::uint32_t>(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    rk0[r] = k0;
+    rk1[r] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+dev_predicate compile_dev_predicate(const std::uint32_t* bits, const std::uint8_t* vals,
+                                    std::uint32_t n, std::uint32_t n_kept) {
+  dev_predicate p{};
+  for (std::uint32_t i = 0; i < n; ++i) {
+    if (bits[i] >= n_kept) throw model_error("predicate references a bit outside the state");
+    const std::uint32_t w = bits[i] >> 5, m = 1u << (bits[i] & 31);
+    std::uint32_t j = 0;
+    while (j < p.n && p.w[j] != w) ++j;
+    if (j == p.n) {
+      if (p.n == kMaxPredWords) throw resource_error("predicate spans too many state words");
+      p.w[j] = w;
+      p.mask[j] = 0;
+      p.want[j] = 0;
+      ++p.n;
+    }
+    if (p.mask[j] & m) {
+      // repeated term: contradictory values make the predicate unsatisfiable
+      if (((p.want[j] & m) != 0) != (vals[i] != 0)) {
+        p.mask[j] |= m;
+        p.want[j] ^= m;  // flip -> can never match both; keep as contradiction marker
+      }
+      continue;
+    }
+    p.mask[j] |= m;
+    if (vals[i]) p.want[j] |= m;
+  }
+  return p;
+}
+
+encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
+  if (lpt == 0 || lpt > 32 || (lpt & (lpt - 1)) != 0)
+    throw model_error("lanes per trajectory must be a power of two in [1, 32]");
+  const std::uint32_t n = v.n_kept;
+  if (n == 0) throw model_error("empty plan");
+  if (n >= 65535) throw resource_error("device engine supports at most 65534 kept nodes");
+  if (v.pert_k < 1 || v.pert_k > 24) throw resource_error("perturbation width must be in [1,24]");
+  if (v.pert_size != (1u << v.pert_k)) throw model_error("perturbation table size != 2^k");
+
+  encoded_plan ep;
+  dev_plan_header& h = ep.h;
+  h.n_kept = n;
+  h.sw32 = 2 * (n / 64 + 1);
+  h.g = v.pert_groups;
+  h.k = v.pert_k;
+  h.last_mask = static_cast<std::uint32_t>(v.pert_mask);
+  h.n_groups = v.n_groups;
+  h.lpt = lpt;
+  // leaf perturbation iff u > t  <=>  r > floor(t * 2^bits) (t*2^bits is exact)
+  const double t53 = std::floor(std::ldexp(v.t, 53));
+  h.leaf_thr53 = static_cast<std::uint64_t>(t53);
+  const double t32 = std::floor(std::ldexp(v.t, 32));
+  h.leaf_never = v.t >= 1.0 ? 1u : 0u;
+  h.leaf_thr32 = t32 >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<std::uint32_t>(t32);
+
+  // ---- perturbation cells
+  const std::uint32_t k = v.pert_k;
+  std::vector<std::uint64_t> pert53(v.pert_size);
+  std::vector<std::uint32_t> pert32(v.pert_size);
+  for (std::uint32_t c = 0; c < v.pert_size; ++c) {
+    const double cut = v.pert_cut[c];
+    const std::uint32_t al = v.pert_alias[c];
+    {
+      const double T = std::ceil(std::ldexp(cut, 53 - static_cast<int>(k)));
+      const double full = std::ldexp(1.0, 53 - static_cast<int>(k));
+      std::uint64_t tt = 0, aa = c;
+      if (T < full) {
+        tt = static_cast<std::uint64_t>(T);
+        aa = al;
+      }
+      pert53[c] = tt | (aa << (53 - k));
+    }
+    {
+      const double T = std::ceil(std::ldexp(cut, 32 - static_cast<int>(k)));
+      const double full = std::ldexp(1.0, 32 - static_cast<int>(k));
+      std::uint32_t tt = 0, aa = c;
+      if (T < full) {
+        tt = static_cast<std::uint32_t>(T);
+        aa = al;
+      }
+      pert32[c] = tt | (aa << (32 - k));
+    }
+  }
+
+  // ---- groups, functions, gather records, tables
+  std::vector<std::uint32_t> groups(4 * static_cast<std::size_t>(v.n_groups));
+  std::vector<std::uint32_t> fns(2 * static_cast<std::size_t>(v.n_fns));
+  std::vector<std::uint16_t> grec;
+  std::vector<std::uint8_t> tables;
+  std::vector<std::uint32_t> fn_members(v.n_fns, 0);
+  h.max_alias = 0;
+  std::vector<std::uint32_t> cost(v.n_groups, 0);
+  for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
+    const std::uint32_t off = v.grp_offset[gi];
+    const std::uint32_t end = gi + 1 < v.n_groups ? v.grp_offset[gi + 1] : n;
+    if (end <= off || end - off > 64) throw model_error("group member count out of range");
+    const std::uint32_t members = end - off;
+    const std::uint32_t asz = v.grp_alias_size[gi];
+    if (asz >= (1u << 23)) throw resource_error("group alias table too large for the device");
+    h.max_alias = std::max(h.max_alias, asz);
+    groups[4 * gi + 0] = off;
+    groups[4 * gi + 1] = v.grp_fn_begin[gi];
+    groups[4 * gi + 2] = v.grp_alias_begin[gi];
+    groups[4 * gi + 3] = asz | ((members - 1) << 24);
+    const std::uint32_t nf = asz ? asz : 1;
+    std::uint32_t max_gc = 0;
+    for (std::uint32_t j = 0; j < nf; ++j) {
+      const std::uint32_t f = v.grp_fn_begin[gi] + j;
+      if (f >= v.n_fns) throw model_error("function index out of range");
+      fn_members[f] = members;
+      max_gc = std::max(max_gc, v.fn_gather_count[f]);
+    }
+    cost[gi] = 3 + (asz ? 4 : 0) + 2 * ((max_gc + 3) / 4);
+  }
+  for (std::uint32_t f = 0; f < v.n_fns; ++f) {
+    const std::uint32_t gc = v.fn_gather_count[f];
+    if (gc > 30) throw resource_error("gather list longer than 30 bits");
+    const std::uint32_t members = fn_members[f] ? fn_members[f] : 1;
+    const std::uint32_t el2 = entry_log2(members);
+    // table
+    std::size_t tb = tables.size();
+    const std::size_t align = el2 == 3 ? 8 : 4;
+    tb = (tb + align - 1) & ~(align - 1);
+    const std::uint64_t len = 1ull << gc;
+    const std::size_t bytes = static_cast<std::size_t>(len) << el2;
+    tables.resize(((tb + bytes) + 3) & ~std::size_t(3), 0);
+    if (v.fn_table_begin[f] + len > v.n_table) throw model_error("table range out of bounds");
+    for (std::uint64_t e = 0; e < len; ++e) {
+      const std::uint64_t out = v.fn_tables[v.fn_table_begin[f] + e];
+      std::memcpy(tables.data() + tb + (e << el2), &out, std::size_t(1) << el2);  // little endian
+    }
+    if (tb > 0xFFFFFFFFull) throw resource_error("function tables exceed 4 GiB");
+    // gather records
+    while (grec.size() % 4) grec.push_back(0);
+    const std::size_t gb = grec.size();
+    if (gb >= (1u << 27)) throw resource_error("too many gather records");
+    const std::uint32_t slots = (gc + 3) & ~3u;
+    if (v.fn_gather_begin[f] + gc > v.n_gather) throw model_error("gather range out of bounds");
+    for (std::uint32_t b = 0; b < slots; ++b) {
+      const std::uint32_t pos = b < gc ? v.fn_gather[v.fn_gather_begin[f] + b] : n;
+      if (pos > n) throw model_error("gather position out of range");
+      grec.push_back(static_cast<std::uint16_t>(((pos >> 5) << 5) | (((pos & 31) - b) & 31)));
+    }
+    fns[2 * f + 0] = static_cast<std::uint32_t>(tb);
+    fns[2 * f + 1] = static_cast<std::uint32_t>(gb << 5) | gc;
+  }
+
+  // ---- group alias cells
+  std::vector<double> acut(v.alias_cut, v.alias_cut + v.n_alias);
+  std::vector<std::uint32_t> aidx(v.alias_idx, v.alias_idx + v.n_alias);
+  std::vector<std::uint32_t> a32(2 * v.n_alias);
+  h.u32_ok = h.max_alias <= (1u << 21) ? 1u : 0u;
+  for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
+    const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
+    if (static_cast<std::uint64_t>(ab) + asz > v.n_alias) throw model_error("alias range out of bounds");
+    for (std::uint32_t c = 0; c < asz; ++c) {
+      const double T = std::ceil(std::ldexp(v.alias_cut[ab + c], 32));
+      std::uint32_t tt = 0, aa = c;
+      if (T < 4294967296.0) {
+        tt = static_cast<std::uint32_t>(T);
+        aa = v.alias_idx[ab + c];
+      }
+      a32[2 * (ab + c) + 0] = tt;
+      a32[2 * (ab + c) + 1] = aa;
+    }
+  }
+
+  // ---- lane buckets: contiguous group ranges balanced by a static cost; a
+  // range that starts inside the alias region starts at an alias ordinal o
+  // with (g + 1 + o) % 4 == 0, so its draws begin on a Philox block boundary
+  // for both streams (2 or 4 draws per block) and lanes refill in lockstep.
+  std::vector<std::uint32_t> buckets(lpt + 1, 0), aord(lpt, 0);
+  {
+    std::vector<std::uint64_t> prefix(v.n_groups + 1, 0);
+    std::vector<std::uint32_t> ord(v.n_groups + 1, 0);
+    for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
+      prefix[gi + 1] = prefix[gi] + cost[gi];
+      ord[gi + 1] = ord[gi] + (v.grp_alias_size[gi] ? 1 : 0);
+    }
+    const std::uint64_t total = prefix[v.n_groups];
+    std::uint32_t b = 0;
+    for (std::uint32_t r = 1; r < lpt; ++r) {
+      const std::uint64_t target = total * r / lpt;
+      while (b < v.n_groups && prefix[b] < target) ++b;
+      // align to a block boundary while inside the alias region
+      while (b < v.n_groups && v.grp_alias_size[b] != 0 && ((v.pert_groups + 1 + ord[b]) % 4) != 0)
+        ++b;
+      buckets[r] = std::max(b, buckets[r - 1]);
+    }
+    buckets[lpt] = v.n_groups;
+    for (std::uint32_t r = 0; r < lpt; ++r) aord[r] = ord[buckets[r]];
+  }
+
+  // ---- assemble
+  std::size_t off = 0;
+  auto section = [&](std::size_t bytes) {
+    const std::size_t o = off;
+    off = align16(off + bytes);
+    return static_cast<std::uint32_t>(o);
+  };
+  h.off_pert53 = section(8 * pert53.size());
+  h.off_pert32 = section(4 * pert32.size());
+  h.off_groups = section(4 * groups.size());
+  h.off_fns = section(4 * fns.size());
+  h.off_grec = section(2 * grec.size());
+  h.off_acut = section(8 * acut.size());
+  h.off_aidx = section(4 * aidx.size());
+  h.off_a32 = section(4 * a32.size());
+  h.off_buckets = section(4 * buckets.size());
+  h.off_aord = section(4 * aord.size());
+  h.core_bytes = static_cast<std::uint32_t>(off);
+  h.off_tables = static_cast<std::uint32_t>(off);
+  h.table_bytes = static_cast<std::uint32_t>(align16(tables.size()));
+  if (off + h.table_bytes > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
+  ep.blob.assign(off + h.table_bytes, 0);
+  put(ep.blob, h.off_pert53, pert53);
+  put(ep.blob, h.off_pert32, pert32);
+  put(ep.blob, h.off_groups, groups);
+  put(ep.blob, h.off_fns, fns);
+  put(ep.blob, h.off_grec, grec);
+  put(ep.blob, h.off_acut, acut);
+  put(ep.blob, h.off_aidx, aidx);
+  put(ep.blob, h.off_a32, a32);
+  put(ep.blob, h.off_buckets, buckets);
+  put(ep.blob, h.off_aord, aord);
+  put(ep.blob, h.off_tables, tables);
+  return ep;
+}
+
+}  // namespace pbn_b200
