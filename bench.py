@@ -1,0 +1,359 @@
+#!/usr/bin/env python3
+"""Throughput benchmark of the PBN trajectory hot path (BASELINE.json metric:
+node-updates/s and trajectory-steps/s; % of the shared-memory lookup roofline).
+
+One bench "step" = one pass of the hot path over the workload: every trajectory
+of the ensemble advanced by the config's step count (c2: 4096 trajectories x
+1e5 steps per GPU), continuing from the previous step's states.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--stream u53|u32]
+  python bench.py --impl reference ...   # the reference's own CPU stepper, all host cores
+
+Multi-GPU (torchrun, one rank per GPU): each rank owns a contiguous range of
+global trajectory ids (weak scaling); the per-trajectory counts are combined
+with ONE NCCL all-reduce at the end; time = max over ranks of device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1605_00854_b200.configs import CONFIGS  # noqa: E402
+
+METRIC = "node-updates/sec"
+UNIT = "node-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--stream", default="u53", choices=["u53", "u32"])
+    ap.add_argument("--p", type=float, default=None, help="override perturbation rate (c5 sweep)")
+    ap.add_argument("--traj", type=int, default=None, help="trajectories per GPU")
+    ap.add_argument("--sim-steps", type=int, default=None, help="simulation steps per bench step")
+    ap.add_argument("--lpt", type=int, default=0)
+    ap.add_argument("--placement", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_workload(cfg, p_override):
+    """Model text is the interchange format: both this library and the
+    reference parse the same text, so their plans are bitwise identical."""
+    import paper_1605_00854_b200 as pb
+
+    w = CONFIGS[cfg]
+    model, terms = w.model(p_override)
+    text = model.serialize()
+    model = pb.parse_model(text)
+    plan = pb.prepare(model, w.theta, w.k_max, w.mgp)
+    return w, text, model, plan, terms
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def cpu_reference_rate(text, w, terms, seconds, threads=None):
+    """The unmodified reference grouped stepper (oracle/_ref, xoshiro256),
+    one trajectory per host thread. Returns (traj-steps/s, threads, sample)."""
+    import oracle
+
+    ref = oracle.Reference()
+    rplan = ref.parse(text).prepare(w.theta, w.k_max, w.mgp)
+    pred = rplan.compile_predicate(terms)
+    threads = threads or os.cpu_count() or 1
+    # calibrate on one thread, then size the sample to ~`seconds`
+    s_cal = 2000
+    t, _ = rplan.bench_xoshiro(42, 1, s_cal, pred)
+    per_step = max(t / s_cal, 1e-9)
+    steps = max(1000, int(seconds / per_step))
+    t, _ = rplan.bench_xoshiro(42, threads, steps, pred)
+    rate = threads * steps / t
+    return rate, threads, steps, t, rplan.n_kept
+
+
+def run_reference_arm(a):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import paper_1605_00854_b200 as pb  # noqa: F401  (model generation / plan only)
+
+    w, text, model, plan, terms = build_workload(a.config, a.p)
+    import oracle
+
+    ref = oracle.Reference()
+    rplan = ref.parse(text).prepare(w.theta, w.k_max, w.mgp)
+    pred = rplan.compile_predicate(terms)
+    threads = os.cpu_count() or 1
+    t, _ = rplan.bench_xoshiro(42, 1, 2000, pred)
+    steps = max(1000, int(6.0 / max(t / 2000, 1e-9)))  # ~6 s per bench step
+    for _ in range(a.warmup):
+        rplan.bench_xoshiro(42, threads, max(1000, steps // 10), pred)
+    times = []
+    for k in range(a.steps):
+        t, _ = rplan.bench_xoshiro(42 + 1000 * k, threads, steps, pred)
+        times.append(t)
+    total = sum(times)
+    tsteps = threads * steps * a.steps
+    val = tsteps * rplan.n_kept / total
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1000 * total / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": rplan.n_kept,
+                   "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
+                   "p": a.p if a.p is not None else w.p},
+        "trajectory_steps_per_s": tsteps / total,
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} threads x {steps} steps, reference grouped_simulator"
+                                   f" + xoshiro256, count_nodes=false, predicate on"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import torch
+
+    import paper_1605_00854_b200 as pb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    w, text, model, plan, terms = build_workload(a.config, a.p)
+    flat = plan.flat()
+    pred = plan.compile_predicate(terms)
+    n_traj = a.traj or w.n_traj
+    sim_steps = a.sim_steps or (w.n_steps if w.n_steps else 100_000)
+    stream = pb.STREAM_U53 if a.stream == "u53" else pb.STREAM_U32
+    eng = pb.GpuEnsemble(plan, device=local, lanes_per_traj=a.lpt, placement=a.placement)
+    words = eng.words
+    traj_begin = rank * n_traj
+
+    states = torch.zeros((n_traj, words), dtype=torch.int64, device=dev)
+    counts = torch.zeros((n_traj, 8), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > L2 (126 MB)
+    cs = torch.cuda.current_stream(dev)
+    step_pos = 0
+
+    def one(n_steps):
+        nonlocal step_pos
+        eng.simulate_device(42, n_traj, n_steps, states.data_ptr(), counts.data_ptr(),
+                            traj_begin=traj_begin, step_begin=step_pos, pred=pred, stream=stream,
+                            cuda_stream=cs.cuda_stream)
+        step_pos += n_steps
+
+    for _ in range(max(a.warmup, 3)):
+        one(max(1, sim_steps // 10))
+    torch.cuda.synchronize(dev)
+
+    fn_steps = 0
+    launches = 0
+    ev_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(a.steps):
+            flush.fill_(k)  # L2 flush between timed iterations (outside the events)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            one(sim_steps)
+            e1.record(cs)
+            launches += eng.last_launches()
+            e1.synchronize()
+            ev_ms.append(e0.elapsed_time(e1))
+            fn_steps += int(counts[:, 6].sum().item())
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    my_ms = sum(ev_ms)
+    t_ms = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([fn_steps], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        # the single collective of the path: one all-reduce of the counts
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    total_ms = float(t_ms.item())
+    fn_total = int(tot.item())
+    traj_steps = n_traj * world * sim_steps * a.steps
+    value = traj_steps * flat.n_kept / (total_ms / 1e3)
+
+    # ---- end to end through the public C-ABI with HOST buffers (pinned),
+    # host<->device copies inside the timed region (pbn_gpu_run is synchronous)
+    host_states = torch.zeros((n_traj, words), dtype=torch.int64).pin_memory()
+    host_counts = torch.zeros((n_traj, 8), dtype=torch.int64).pin_memory()
+    import ctypes as C
+
+    def e2e_one(n_steps, s0):
+        args = eng._args(42, traj_begin, n_traj, n_steps, s0, pred, stream)
+        pb._check(pb.lib.pbn_gpu_run(eng._h, C.byref(args),
+                                     C.cast(host_states.data_ptr(), C.POINTER(C.c_uint64)),
+                                     C.cast(host_counts.data_ptr(), C.POINTER(C.c_uint64)), None))
+
+    e2e_one(max(1, sim_steps // 10), 0)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(a.steps):
+        e2e_one(sim_steps, k * sim_steps)
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = traj_steps * flat.n_kept / float(e2e_t.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    props = torch.cuda.get_device_properties(dev)
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_lookups = props.multi_processor_count * 32 * sm_mhz * 1e6
+    lookups = flat.expected_lookups(fn_total, traj_steps)
+    achieved = lookups / (total_ms / 1e3) / world
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": max(a.warmup, 3), "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": flat.n_kept,
+                   "trajectories_per_gpu": n_traj, "sim_steps_per_bench_step": sim_steps,
+                   "p": a.p if a.p is not None else w.p,
+                   "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
+                   "stream": a.stream, "engine": eng.info(),
+                   "l2": "flushed between timed iterations (256 MiB write)",
+                   "parallelism": f"trajectory-sharded x{world}"},
+        "trajectory_steps_per_s": traj_steps / (total_ms / 1e3),
+        "node_updates_per_s_original_n": traj_steps * w.n / (total_ms / 1e3),
+        "fn_phase_fraction": fn_total / traj_steps,
+        "e2e": {"value": e2e_val, "unit": UNIT,
+                "h2d_bytes_per_step": n_traj * words * 8,
+                "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
+        "gpu_launches": launches,
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
+                     "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": None,
+                     "note": "lookup roofline = SMs x 32 probes/clk x sm_max_mhz "
+                             "(MEASURED_PEAKS.json); algorithmic lookups = g per step + "
+                             "(A+G) per function-phase step (SURVEY 8d), per GPU",
+                     "lookups_per_step": lookups / traj_steps},
+        "clocks": clk.summary(),
+    }
+    if not a.no_cpu_baseline and world == 1:
+        try:
+            rate, threads, steps, secs, nk = cpu_reference_rate(text, w, terms, a.cpu_seconds)
+            line["cpu_baseline"] = {
+                "value": rate * nk, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{threads} threads x {steps} steps ({secs:.1f} s), unmodified reference "
+                          f"grouped_simulator + xoshiro256 (oracle/_ref)",
+                "trajectory_steps_per_s": rate}
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

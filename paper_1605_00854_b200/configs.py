@@ -2,7 +2,7 @@
 
 The paper's corpus and the apoptosis network are not available,
 so seeded BASELINE-shaped networks stand in: model seed
-1605 + config index, simulation seed 42, all-zero initial states.
+1605 + 0-based config index, simulation seed 42, all-zero initial states.
 
 Plan parameters (theta, k_max, max_group_parents) are part of the workload and
 are passed identically to the oracle / reference: bit-exactness needs the same
@@ -42,15 +42,15 @@ class Workload:
 
 
 CONFIGS = {
-    "c1": Workload("c1", 100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1606, 4096, 1_000_000,
+    "c1": Workload("c1", 100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 4096, 1_000_000,
                    note="n=100, target node0=1 AND node1=1; CPU ref 1 traj x 1e6 steps"),
-    "c2": Workload("c2", 1000, (1, 5), (1, 4), 0.001, 0.0, 3, False, 1607, 4096, 100_000,
+    "c2": Workload("c2", 1000, (1, 5), (1, 4), 0.001, 0.0, 3, False, 1606, 4096, 100_000,
                    note="n=1000, 4096 trajectories x 1e5 steps, single B200 (headline)"),
-    "c3": Workload("c3", 96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1608, 65536, 0,
+    "c3": Workload("c3", 96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607, 65536, 0,
                    note="n=96 dense, ~30% leaves; two-state MC estimate r=1e-3, conf 0.95"),
-    "c4": Workload("c4", 5000, (1, 4), (1, 5), 0.0001, 0.0, 2, False, 1609, 16384, 100_000,
+    "c4": Workload("c4", 5000, (1, 4), (1, 5), 0.0001, 0.0, 2, False, 1608, 16384, 100_000,
                    mgp=12, note="n=5000, merged tables up to 2^12 entries (spill), 8 GPUs"),
-    "c5": Workload("c5", 2000, (1, 3), (1, 4), 0.01, 0.0, 2, False, 1610, 32768, 1_000_000,
+    "c5": Workload("c5", 2000, (1, 3), (1, 4), 0.01, 0.0, 2, False, 1609, 32768, 1_000_000,
                    sweep=(0.1, 0.01, 0.001, 0.0001),
                    note="n=2000 perturbation sweep, 32768 traj x 1e6 steps per GPU"),
 }

@@ -12,11 +12,11 @@ pytestmark = pytest.mark.gpu
 
 CASES = {
     # name: (n, F, P, p, leaf, n_targets, fixed, seed, k, mgp)
-    "c1": (100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1606, 12, 8),
-    "c2": (1000, (1, 5), (1, 4), 0.001, 0.0, 3, False, 1607, 12, 8),
-    "c3": (96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1608, 12, 8),
-    "c5": (2000, (1, 3), (1, 4), 0.01, 0.0, 2, False, 1610, 12, 8),
-    "c1_k16": (100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1606, 16, 12),
+    "c1": (100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 12, 8),
+    "c2": (1000, (1, 5), (1, 4), 0.001, 0.0, 3, False, 1606, 12, 8),
+    "c3": (96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607, 12, 8),
+    "c5": (2000, (1, 3), (1, 4), 0.01, 0.0, 2, False, 1609, 12, 8),
+    "c1_k16": (100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 16, 12),
     "tiny": (6, (1, 3), (1, 3), 0.25, 0.0, 2, False, 7, 3, 18),
 }
 
