@@ -83,7 +83,7 @@ class Oracle:
         L.orc_philox_block.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                        C.POINTER(C.c_uint32)]
         L.orc_draw.restype = C.c_double
-        L.orc_draw.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int]
+        L.orc_draw.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_uint32]
 
     def simulate(self, view, seed, traj_begin, n_traj, n_steps, states=None, step_begin=0,
                  pred=None, stream=0, node_counts=False):
@@ -116,8 +116,8 @@ class Oracle:
         self.lib.orc_philox_block(_u32p(c), _u32p(k), _u32p(out))
         return out
 
-    def draw(self, seed, traj, step, d, stream=0):
-        return self.lib.orc_draw(seed, traj, step, d, stream)
+    def draw(self, seed, traj, step, d, stream=0, g=0):
+        return self.lib.orc_draw(seed, traj, step, d, stream, g)
 
 
 # ---------------------------------------------------------------------------

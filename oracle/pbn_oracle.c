@@ -116,7 +116,7 @@ int orc_simulate(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, uin
     memset(cnt, 0, sizeof(uint64_t) * PBN_COUNT_FIELDS);
     if (nc) memset(nc, 0, sizeof(uint64_t) * v->n_kept);
     orc_stream rng;
-    orc_stream_init(&rng, seed, (uint32_t)(traj_begin + t), stream_kind);
+    orc_stream_init(&rng, seed, (uint32_t)(traj_begin + t), stream_kind, v->pert_groups);
     int prev = n_pred ? orc_pred(s, pred_bits, pred_vals, n_pred) : 0;
     for (uint64_t k = 0; k < n_steps; ++k) {
       orc_stream_begin_step(&rng, step_begin + k);
@@ -185,10 +185,11 @@ void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
   orc_philox4x32_10(ctr, key, out);
 }
 
-/* Draw d of (seed, traj, step) as a double, exported for stream tests. */
-double orc_draw(uint64_t seed, uint32_t traj, uint64_t step, uint64_t d, int kind) {
+/* Draw d of (seed, traj, step) as a double for a plan with g perturbation
+ * groups, exported for stream tests. */
+double orc_draw(uint64_t seed, uint32_t traj, uint64_t step, uint64_t d, int kind, uint32_t g) {
   orc_stream s;
-  orc_stream_init(&s, seed, traj, kind);
+  orc_stream_init(&s, seed, traj, kind, g);
   orc_stream_begin_step(&s, step);
   const uint64_t r = orc_stream_raw(&s, d);
   return kind == 0 ? (double)r * 0x1.0p-53 : (double)r * 0x1.0p-32;

@@ -16,7 +16,13 @@
  *   U53: 2 draws per block, draw e in {0,1}: ((x[2e+1] << 32 | x[2e]) >> 11) * 2^-53
  *        — the same 53-bit conversion as xoshiro256::next_double (rng.hpp:35)
  *   U32: 4 draws per block, draw e in {0..3}: x[e] * 2^-32
- *   draw d of a step lives in block d / DPB at position d % DPB.
+ *   Within a step the draws come in two phases (engine.hpp:255-312):
+ *     phase A = draws 0..g (the g grouped-perturbation draws and the leaf draw):
+ *               draw d lives in block d / DPB at position d % DPB;
+ *     phase B = the function-selection draws of the alias groups, j = d - (g+1):
+ *               block NB0 + j / DPB, position j % DPB, NB0 = ceil((g+1) / DPB),
+ *     i.e. phase B starts on a fresh block, so the device can prefetch its
+ *     draws in whole blocks. g is the plan's perturbation group count.
  */
 #ifndef PBN_ORACLE_PHILOX_STREAM_H
 #define PBN_ORACLE_PHILOX_STREAM_H
@@ -52,12 +58,18 @@ typedef struct orc_stream {
   uint64_t step;
   uint64_t d;        /* draws consumed in the current step */
   int kind;          /* 0 = U53, 1 = U32 */
+  uint64_t g1;       /* phase-A draws per step: g + 1 */
+  uint64_t nb0;      /* first phase-B block: ceil(g1 / DPB) */
   uint64_t cached_block;
   int have_block;
   uint32_t x[4];
 } orc_stream;
 
-static inline void orc_stream_init(orc_stream* s, uint64_t seed, uint32_t traj, int kind) {
+static inline void orc_stream_init(orc_stream* s, uint64_t seed, uint32_t traj, int kind,
+                                   uint32_t g) {
+  const uint64_t dpb = kind == 0 ? 2 : 4;
+  s->g1 = (uint64_t)g + 1;
+  s->nb0 = (s->g1 + dpb - 1) / dpb;
   s->seed = seed;
   s->traj = traj;
   s->step = 0;
@@ -76,7 +88,8 @@ static inline void orc_stream_begin_step(orc_stream* s, uint64_t step) {
 /* Raw draw d of the current step as an integer: r53 (U53) or r32 (U32). */
 static inline uint64_t orc_stream_raw(orc_stream* s, uint64_t d) {
   const uint64_t dpb = s->kind == 0 ? 2 : 4;
-  const uint64_t b = d / dpb;
+  const uint64_t b = d < s->g1 ? d / dpb : s->nb0 + (d - s->g1) / dpb;
+  const unsigned e = (unsigned)(d < s->g1 ? d % dpb : (d - s->g1) % dpb);
   if (!s->have_block || s->cached_block != b) {
     const uint32_t ctr[4] = {s->traj, (uint32_t)b, (uint32_t)s->step, (uint32_t)(s->step >> 32)};
     const uint32_t key[2] = {(uint32_t)s->seed, (uint32_t)(s->seed >> 32)};
@@ -84,7 +97,6 @@ static inline uint64_t orc_stream_raw(orc_stream* s, uint64_t d) {
     s->cached_block = b;
     s->have_block = 1;
   }
-  const unsigned e = (unsigned)(d % dpb);
   if (s->kind == 0) return (((uint64_t)s->x[2 * e + 1] << 32) | s->x[2 * e]) >> 11;
   return s->x[e];
 }

@@ -253,7 +253,8 @@ int ref_simulate_philox(void* p, std::uint64_t seed, std::uint64_t traj_begin,
         ws.prev = pbn::eval_predicate(cp, s) ? 1 : 0;
       }
       philox_rng rng;
-      orc_stream_init(&rng.st, seed, static_cast<std::uint32_t>(traj_begin + t), kind);
+      orc_stream_init(&rng.st, seed, static_cast<std::uint32_t>(traj_begin + t), kind,
+                      ps.pplan.groups);
       rng.next_step = step_begin;
       pbn::sim_options opt;
       opt.count_nodes = node_counts != nullptr;
@@ -369,7 +370,7 @@ int ref_estimate(void* p, const std::uint32_t* pred_nodes, const std::uint8_t* p
     } else {
       wrapped_stepper ws(ps);
       philox_rng rng;
-      orc_stream_init(&rng.st, seed, traj, kind);
+      orc_stream_init(&rng.st, seed, traj, kind, ps.pplan.groups);
       r = pbn::estimate_steady_state(ws, s, cp, req, rng);
     }
     *estimate = r.estimate;

@@ -113,7 +113,8 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj) {
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(32, w));
-  const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * 2 * g.ep.h.sw32 * 4;
+  const std::uint64_t stride = (2 * g.ep.h.sw32 + lpt * 4 + 3) & ~3u;
+  const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
   const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
   while (w > 1 && w * per_warp > avail) --w;
   if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");

@@ -11,12 +11,18 @@
 //                      T = ceil(cut * 2^(53-k)); cells whose cut rounds to the
 //                      whole range store (T=0, alias=c).
 //   pert32[2^k]   u32  the same for the U32 stream with 32-k threshold bits.
-//   groups[G]     uint4 {offset, fn_begin, alias_begin, alias_size | (members-1)<<24}
-//   fns[F]        uint2 {table byte offset, (gather record start << 5) | gather count}
-//   grec[...]     u16  gather records, 4-aligned per function, padded with the
-//                      always-zero bit n' (engine.hpp:149-150):
-//                      (word32 << 5) | ((bit32 - slot) & 31) — a funnel rotate
-//                      by the low 5 bits lands the parent bit at `slot`.
+//   groups[G]     uint4 {offset, fn_begin, alias_begin, alias_size | (members-1)<<24};
+//                      the A alias groups come first (grouping.hpp: multi-function
+//                      groups precede single-function ones), so the function phase
+//                      runs an alias region [0, A) and a plain region [A, G).
+//   fns[F]        uint4 {table byte offset,
+//                        gather count | entry log2 << 5 | extra-record quad << 8,
+//                        records 0,1 (u16 each), records 2,3}
+//   grec[...]     u16  gather records 4.. of functions with more than 4 parents,
+//                      4-aligned per function. A record is
+//                      (word32 << 5) | ((bit32 - slot) & 31): a funnel rotate by the
+//                      low 5 bits lands the parent bit at `slot`. Unused slots hold
+//                      the always-zero bit n' (engine.hpp:149-150).
 //   acut[A]       f64  group alias cut-offs (U53 path, FP64 like engine.hpp:285-290)
 //   aidx[A]       u32  group alias targets
 //   a32[A]        uint2 {ceil(cut * 2^32) or 0, alias or self}: U32 integer path
@@ -48,6 +54,7 @@ struct dev_plan_header {
   std::uint32_t core_bytes;   // bytes [0, off_tables)
   std::uint32_t table_bytes;  // bytes [off_tables, off_tables + table_bytes)
   std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
+  std::uint32_t n_alias_groups;  // A: groups [0, A) draw a combined function
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

@@ -121,6 +121,15 @@ __device__ __forceinline__ std::uint32_t pert_draw32(const std::uint32_t* cells,
   return (r & lmask) < (e & lmask) ? c : (e >> (32 - k));
 }
 
+// Gather 4 parent bits (records r0..r3 packed in two words) into slots b0..b0+3.
+__device__ __forceinline__ std::uint32_t gather4(const std::uint32_t* S, std::uint32_t p01,
+                                                 std::uint32_t p23, std::uint32_t b0) {
+  const std::uint32_t r0 = p01 & 0xFFFFu, r1 = p01 >> 16, r2 = p23 & 0xFFFFu, r3 = p23 >> 16;
+  const std::uint32_t w0 = S[r0 >> 5], w1 = S[r1 >> 5], w2 = S[r2 >> 5], w3 = S[r3 >> 5];
+  return (__funnelshift_r(w0, w0, r0) & (1u << b0)) | (__funnelshift_r(w1, w1, r1) & (2u << b0)) |
+         (__funnelshift_r(w2, w2, r2) & (4u << b0)) | (__funnelshift_r(w3, w3, r3) & (8u << b0));
+}
+
 template <int LPT, int STREAM, int PLACE>
 __global__ void __launch_bounds__(1024, 1)
     pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
@@ -142,15 +151,11 @@ __global__ void __launch_bounds__(1024, 1)
   const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(core + h.off_pert53);
   const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(core + h.off_pert32);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
-  const uint2* fns = reinterpret_cast<const uint2*>(core + h.off_fns);
+  const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
   const double* acut = reinterpret_cast<const double*>(core + h.off_acut);
   const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(core + h.off_aidx);
   const uint2* a32 = reinterpret_cast<const uint2*>(core + h.off_a32);
-  const std::uint32_t* buckets = reinterpret_cast<const std::uint32_t*>(core + h.off_buckets);
-  const std::uint32_t* aord = reinterpret_cast<const std::uint32_t*>(core + h.off_aord);
-  const std::uint32_t* tab32 = reinterpret_cast<const std::uint32_t*>(tab);
-  const std::uint64_t* tab64 = reinterpret_cast<const std::uint64_t*>(tab);
 
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t r = lane % LPT;
@@ -162,10 +167,15 @@ __global__ void __launch_bounds__(1024, 1)
   const std::uint64_t tloc = static_cast<std::uint64_t>(blockIdx.x) * slots + slot;
   if (tloc >= rp.n_traj) return;
 
+  // per-trajectory shared memory: two state buffers + the phase-B draw buffer
   const std::uint32_t sw32 = h.sw32;
-  std::uint32_t* st_area = reinterpret_cast<std::uint32_t*>(smem + staged);
-  std::uint32_t* S0 = st_area + static_cast<std::size_t>(slot) * 2 * sw32;
+  constexpr std::uint32_t kBuf = LPT * 4;  // LPT Philox blocks of 4 words
+  const std::uint32_t stride = (2 * sw32 + kBuf + 3) & ~3u;
+  std::uint32_t* S0 = reinterpret_cast<std::uint32_t*>(smem + staged) +
+                      static_cast<std::size_t>(slot) * stride;
   std::uint32_t* S1 = S0 + sw32;
+  std::uint32_t* dbuf = S0 + 2 * sw32;
+  dbuf = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(dbuf) + 15) & ~std::uintptr_t(15));
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
     for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w];
@@ -173,9 +183,8 @@ __global__ void __launch_bounds__(1024, 1)
   __syncwarp(smask);
 
   const std::uint32_t k = h.k, g = h.g;
-  const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks holding draws 0..g
-  const std::uint32_t gb0 = ldp<GC>(buckets + r), gb1 = ldp<GC>(buckets + r + 1);
-  const std::uint32_t ord0 = ldp<GC>(aord + r);
+  const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks of phase A = draws 0..g
+  const std::uint32_t A = h.n_alias_groups, NG = h.n_groups;
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
   mulhilo(kPhiloxM0, traj, thi0, tlo0);
@@ -187,6 +196,85 @@ __global__ void __launch_bounds__(1024, 1)
     return ok;
   };
 
+  // One group of the function phase (engine.hpp:281-310): combined-function
+  // choice, gather of its own parents, table lookup. Returns the packed member
+  // outputs; `off`/`members` describe where they go.
+  auto eval_group = [&](const std::uint32_t* Sc, std::uint32_t gi, std::uint32_t jj,
+                        std::uint32_t& olo, std::uint32_t& ohi, std::uint32_t& off,
+                        std::uint32_t& members) {
+    const uint4 G = ldp<GC>(groups + gi);
+    const std::uint32_t asz = G.w & 0x7FFFFFu;
+    members = (G.w >> 24) + 1;
+    off = G.x;
+    std::uint32_t idx = 0;
+    if (asz != 0) {
+      if constexpr (STREAM == STREAM_U53) {
+        // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
+        // contraction, exactly as engine.hpp:285-290 computes it.
+        const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+        const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
+        const double xx = __dmul_rn(u, __uint2double_rn(asz));
+        std::uint32_t c = __double2uint_rz(xx);
+        if (c >= asz) c = asz - 1;
+        const double fr = __dsub_rn(xx, __uint2double_rn(c));
+        idx = fr < ldp<GC>(acut + G.z + c) ? c : ldp<GC>(aidx + G.z + c);
+      } else {
+        // x*N < 2^53 is exact, so floor and fraction are the product's halves
+        const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
+        const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
+        const uint2 cell = ldp<GC>(a32 + G.z + c);
+        idx = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
+      }
+    }
+    const uint4 F = ldp<GC>(fns + G.y + idx);
+    const std::uint32_t gc = F.y & 31u;
+    std::uint32_t v = gather4(Sc, F.z, F.w, 0);
+    if (gc > 4) {
+      const std::uint32_t xq = F.y >> 8;
+      for (std::uint32_t q = 4; q < gc; q += 4) {
+        const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+        v |= gather4(Sc, rr.x, rr.y, q);
+      }
+    }
+    const std::uint32_t el2 = (F.y >> 5) & 3u;
+    ohi = 0;
+    if (el2 == 0) {
+      olo = ldp<GT>(tab + F.x + v);
+    } else if (el2 == 1) {
+      olo = ldp<GT>(reinterpret_cast<const std::uint16_t*>(tab + F.x) + v);
+    } else if (el2 == 2) {
+      olo = ldp<GT>(reinterpret_cast<const std::uint32_t*>(tab + F.x) + v);
+    } else {
+      const uint2 o = ldp<GT>(reinterpret_cast<const uint2*>(tab + F.x) + v);
+      olo = o.x;
+      ohi = o.y;
+    }
+  };
+
+  // OR one round's outputs into the next state (engine.hpp:304-309). A round
+  // of single-node groups covers consecutive bits: one ballot builds the word.
+  auto emit_round = [&](std::uint32_t* Sn, bool act, std::uint32_t olo, std::uint32_t ohi,
+                        std::uint32_t off, std::uint32_t members) {
+    const bool single = __all_sync(smask, !act || members == 1);
+    if (single) {
+      std::uint32_t bits = __ballot_sync(smask, act && (olo & 1u));
+      if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
+      if (r == 0 && bits) {
+        const std::uint32_t w = off >> 5, sh = off & 31;
+        atomicOr(Sn + w, bits << sh);
+        if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
+      }
+    } else if (act) {
+      const std::uint32_t w = off >> 5, sh = off & 31;
+      const std::uint32_t a0 = olo << sh;
+      const std::uint32_t a1 = sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
+      const std::uint32_t a2 = sh ? (ohi >> (32 - sh)) : 0u;
+      if (a0) atomicOr(Sn + w, a0);
+      if (a1) atomicOr(Sn + w + 1, a1);
+      if (a2) atomicOr(Sn + w + 2, a2);
+    }
+  };
+
   std::uint32_t cur = 0;
   std::uint32_t prev = pred_eval(S0);
   std::uint32_t n01 = 0, n10 = 0, n11 = 0, nfn = 0, npert = 0;
@@ -196,7 +284,7 @@ __global__ void __launch_bounds__(1024, 1)
     std::uint32_t* Sc = cur ? S1 : S0;
     const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
 
-    // ---- grouped perturbation + leaf draw (draws 0..g)
+    // ---- phase A: grouped perturbation + leaf draw (draws 0..g)
     bool flip = false, leaf = false;
     for (std::uint32_t b = r; b < nb0; b += LPT) {
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
@@ -210,7 +298,7 @@ __global__ void __launch_bounds__(1024, 1)
           else
             c = pert_draw32<GC>(pert32, pick32(x, e), k);
           if (d + 1 == g) c &= h.last_mask;
-          if (c != 0) {  // xor_chunk (bitstate.hpp:50-58); rare
+          if (c != 0) {  // xor_chunk (bitstate.hpp:50-58)
             flip = true;
             const std::uint32_t o = d * k, w = o >> 5, sh = o & 31;
             atomicXor(Sc + w, c << sh);
@@ -231,88 +319,37 @@ __global__ void __launch_bounds__(1024, 1)
       __syncwarp(smask);
       ++npert;
     } else if (!any_leaf) {
-      // ---- function phase
+      // ---- function phase, in lockstep rounds of LPT groups
       std::uint32_t* Sn = cur ? S0 : S1;
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
-      __syncwarp(smask);
-      std::uint32_t a0 = 0, a1 = 0, a2 = 0;
-      std::uint32_t cw = gb0 < gb1 ? (ldp<GC>(groups + gb0).x >> 5) : 0;
-      std::uint32_t ord = ord0;
-      std::uint32_t bcached = 0xFFFFFFFFu;
-      uint4 bx = make_uint4(0, 0, 0, 0);
-      for (std::uint32_t gi = gb0; gi < gb1; ++gi) {
-        const uint4 G = ldp<GC>(groups + gi);
-        const std::uint32_t asz = G.w & 0x7FFFFFu;
-        const std::uint32_t members = (G.w >> 24) + 1;
-        std::uint32_t idx = 0;
-        if (asz != 0) {
-          const std::uint32_t d = g + 1 + ord;
-          ++ord;
-          const std::uint32_t blk = d / DPB, e = d % DPB;
-          if (blk != bcached) {
-            bx = philox_block(sp, blk, rp.rk0, rp.rk1);
-            bcached = blk;
-          }
-          if constexpr (STREAM == STREAM_U53) {
-            // u*N, truncation, clamp, fraction vs cut-off — in IEEE double
-            // without contraction, as engine.hpp:285-290 computes it.
-            const double u = __ull2double_rn(pick53(bx, e).value()) * 0x1.0p-53;
-            const double xx = __dmul_rn(u, __uint2double_rn(asz));
-            std::uint32_t c = __double2uint_rz(xx);
-            if (c >= asz) c = asz - 1;
-            const double fr = __dsub_rn(xx, __uint2double_rn(c));
-            idx = fr < ldp<GC>(acut + G.z + c) ? c : ldp<GC>(aidx + G.z + c);
-          } else {
-            const std::uint64_t P = static_cast<std::uint64_t>(pick32(bx, e)) * asz;
-            const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
-            const uint2 cell = ldp<GC>(a32 + G.z + c);
-            idx = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
-          }
+      // alias region: chunks of LPT*DPB draws; lane r first computes phase-B
+      // block nb0 + j0/DPB + r into the draw buffer
+      for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB) {
+        if (j0 + r * DPB < A) {
+          const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
+          *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
         }
-        const uint2 F = ldp<GC>(fns + G.y + idx);
-        const std::uint32_t gc = F.y & 31u;
-        const std::uint32_t rb = F.y >> 7;  // record quad index (records are 4-aligned)
-        std::uint32_t v = 0;
-        for (std::uint32_t j = 0; j < gc; j += 4) {
-          const uint2 q = ldp<GC>(grec + rb + (j >> 2));
-          const std::uint32_t r0 = q.x & 0xFFFFu, r1 = q.x >> 16, r2 = q.y & 0xFFFFu,
-                              r3 = q.y >> 16;
-          const std::uint32_t w0 = Sc[r0 >> 5], w1 = Sc[r1 >> 5], w2 = Sc[r2 >> 5],
-                              w3 = Sc[r3 >> 5];
-          v |= (__funnelshift_r(w0, w0, r0) & (1u << j)) |
-               (__funnelshift_r(w1, w1, r1) & (2u << j)) |
-               (__funnelshift_r(w2, w2, r2) & (4u << j)) |
-               (__funnelshift_r(w3, w3, r3) & (8u << j));
+        __syncwarp(smask);
+#pragma unroll
+        for (std::uint32_t t = 0; t < DPB; ++t) {
+          const std::uint32_t jr = j0 + t * LPT;
+          if (jr >= A) break;
+          const std::uint32_t j = jr + r;
+          const bool act = j < A;
+          std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
+          if (act) eval_group(Sc, j, t * LPT + r, olo, ohi, off, members);
+          emit_round(Sn, act, olo, ohi, off, members);
         }
-        // table lookup (engine.hpp:303), entries of 1/2/4/8 bytes
-        std::uint32_t olo, ohi = 0;
-        if (members <= 32) {
-          const std::uint32_t el2 = members <= 8 ? 0 : members <= 16 ? 1 : 2;
-          const std::uint32_t addr = F.x + (v << el2);
-          const std::uint32_t word = ldp<GT>(tab32 + (addr >> 2));
-          const std::uint32_t m = members == 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
-          olo = (word >> ((addr & 3u) << 3)) & m;
-        } else {
-          const std::uint64_t o64 = ldp<GT>(tab64 + (F.x >> 3) + v);
-          olo = static_cast<std::uint32_t>(o64);
-          ohi = static_cast<std::uint32_t>(o64 >> 32);
-        }
-        // OR into the next state at the group offset (engine.hpp:304-309)
-        const std::uint32_t w = G.x >> 5, sh = G.x & 31;
-        while (cw < w) {
-          if (a0) atomicOr(Sn + cw, a0);
-          a0 = a1;
-          a1 = a2;
-          a2 = 0;
-          ++cw;
-        }
-        a0 |= olo << sh;
-        a1 |= sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
-        a2 |= sh ? (ohi >> (32 - sh)) : 0u;
+        __syncwarp(smask);
       }
-      if (a0) atomicOr(Sn + cw, a0);
-      if (a1) atomicOr(Sn + cw + 1, a1);
-      if (a2) atomicOr(Sn + cw + 2, a2);
+      // plain region (one combined function per group, no draw)
+      for (std::uint32_t gr = A; gr < NG; gr += LPT) {
+        const std::uint32_t gi = gr + r;
+        const bool act = gi < NG;
+        std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
+        if (act) eval_group(Sc, gi, 0, olo, ohi, off, members);
+        emit_round(Sn, act, olo, ohi, off, members);
+      }
       __syncwarp(smask);
       cur ^= 1;
       ++nfn;
@@ -407,7 +444,8 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
   std::size_t staged = 0;
   if (place == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
   if (place == PLACE_CORE) staged = h.core_bytes;
-  const std::size_t smem = staged + static_cast<std::size_t>(slots) * 2 * h.sw32 * 4;
+  const std::size_t stride = (2 * h.sw32 + h.lpt * 4 + 3) & ~3u;
+  const std::size_t smem = staged + static_cast<std::size_t>(slots) * stride * 4 + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

@@ -38,6 +38,7 @@ void philox_round_keys(std::uint64_t seed, std::uint32_t rk0[10], std::uint32_t 
 dev_predicate compile_dev_predicate(const std::uint32_t* bits, const std::uint8_t* vals,
                                     std::uint32_t n, std::uint32_t n_kept) {
   dev_predicate p{};
+  bool contradiction = false;
   for (std::uint32_t i = 0; i < n; ++i) {
     if (bits[i] >= n_kept) throw model_error("predicate references a bit outside the state");
     const std::uint32_t w = bits[i] >> 5, m = 1u << (bits[i] & 31);
@@ -50,16 +51,17 @@ dev_predicate compile_dev_predicate(const std::uint32_t* bits, const std::uint8_
       p.want[j] = 0;
       ++p.n;
     }
-    if (p.mask[j] & m) {
-      // repeated term: contradictory values make the predicate unsatisfiable
-      if (((p.want[j] & m) != 0) != (vals[i] != 0)) {
-        p.mask[j] |= m;
-        p.want[j] ^= m;  // flip -> can never match both; keep as contradiction marker
-      }
-      continue;
-    }
+    const std::uint32_t want = vals[i] ? m : 0u;
+    if ((p.mask[j] & m) && (p.want[j] & m) != want) contradiction = true;
     p.mask[j] |= m;
-    if (vals[i]) p.want[j] |= m;
+    p.want[j] |= want;
+  }
+  if (contradiction) {  // "x == 0 and x == 1": never satisfied
+    p = dev_predicate{};
+    p.n = 1;
+    p.w[0] = 0;
+    p.mask[0] = 0;
+    p.want[0] = 1;
   }
   return p;
 }
@@ -120,12 +122,13 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
 
   // ---- groups, functions, gather records, tables
   std::vector<std::uint32_t> groups(4 * static_cast<std::size_t>(v.n_groups));
-  std::vector<std::uint32_t> fns(2 * static_cast<std::size_t>(v.n_fns));
+  std::vector<std::uint32_t> fns(4 * static_cast<std::size_t>(v.n_fns));
   std::vector<std::uint16_t> grec;
   std::vector<std::uint8_t> tables;
   std::vector<std::uint32_t> fn_members(v.n_fns, 0);
   h.max_alias = 0;
-  std::vector<std::uint32_t> cost(v.n_groups, 0);
+  h.n_alias_groups = 0;
+  bool plain_seen = false;
   for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
     const std::uint32_t off = v.grp_offset[gi];
     const std::uint32_t end = gi + 1 < v.n_groups ? v.grp_offset[gi + 1] : n;
@@ -133,24 +136,35 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
     const std::uint32_t members = end - off;
     const std::uint32_t asz = v.grp_alias_size[gi];
     if (asz >= (1u << 23)) throw resource_error("group alias table too large for the device");
+    if (asz == 1) throw model_error("alias table of one cell");
+    if (asz) {
+      if (plain_seen) throw model_error("alias groups must precede single-function groups");
+      ++h.n_alias_groups;
+    } else {
+      plain_seen = true;
+    }
     h.max_alias = std::max(h.max_alias, asz);
     groups[4 * gi + 0] = off;
     groups[4 * gi + 1] = v.grp_fn_begin[gi];
     groups[4 * gi + 2] = v.grp_alias_begin[gi];
     groups[4 * gi + 3] = asz | ((members - 1) << 24);
     const std::uint32_t nf = asz ? asz : 1;
-    std::uint32_t max_gc = 0;
     for (std::uint32_t j = 0; j < nf; ++j) {
       const std::uint32_t f = v.grp_fn_begin[gi] + j;
       if (f >= v.n_fns) throw model_error("function index out of range");
       fn_members[f] = members;
-      max_gc = std::max(max_gc, v.fn_gather_count[f]);
     }
-    cost[gi] = 3 + (asz ? 4 : 0) + 2 * ((max_gc + 3) / 4);
   }
+  auto record = [&](std::uint32_t f, std::uint32_t b) -> std::uint16_t {
+    const std::uint32_t gc = v.fn_gather_count[f];
+    const std::uint32_t pos = b < gc ? v.fn_gather[v.fn_gather_begin[f] + b] : n;
+    if (pos > n) throw model_error("gather position out of range");
+    return static_cast<std::uint16_t>(((pos >> 5) << 5) | (((pos & 31) - b) & 31));
+  };
   for (std::uint32_t f = 0; f < v.n_fns; ++f) {
     const std::uint32_t gc = v.fn_gather_count[f];
     if (gc > 30) throw resource_error("gather list longer than 30 bits");
+    if (v.fn_gather_begin[f] + gc > v.n_gather) throw model_error("gather range out of bounds");
     const std::uint32_t members = fn_members[f] ? fn_members[f] : 1;
     const std::uint32_t el2 = entry_log2(members);
     // table
@@ -166,20 +180,21 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
       std::memcpy(tables.data() + tb + (e << el2), &out, std::size_t(1) << el2);  // little endian
     }
     if (tb > 0xFFFFFFFFull) throw resource_error("function tables exceed 4 GiB");
-    // gather records
-    while (grec.size() % 4) grec.push_back(0);
-    const std::size_t gb = grec.size();
-    if (gb >= (1u << 27)) throw resource_error("too many gather records");
-    const std::uint32_t slots = (gc + 3) & ~3u;
-    if (v.fn_gather_begin[f] + gc > v.n_gather) throw model_error("gather range out of bounds");
-    for (std::uint32_t b = 0; b < slots; ++b) {
-      const std::uint32_t pos = b < gc ? v.fn_gather[v.fn_gather_begin[f] + b] : n;
-      if (pos > n) throw model_error("gather position out of range");
-      grec.push_back(static_cast<std::uint16_t>(((pos >> 5) << 5) | (((pos & 31) - b) & 31)));
+    // records 0..3 inline, the rest in grec (4-aligned quads)
+    std::uint32_t xq = 0;
+    if (gc > 4) {
+      while (grec.size() % 4) grec.push_back(0);
+      xq = static_cast<std::uint32_t>(grec.size() / 4);
+      if (xq >= (1u << 24)) throw resource_error("too many gather records");
+      const std::uint32_t slots = (gc + 3) & ~3u;
+      for (std::uint32_t b = 4; b < slots; ++b) grec.push_back(record(f, b));
     }
-    fns[2 * f + 0] = static_cast<std::uint32_t>(tb);
-    fns[2 * f + 1] = static_cast<std::uint32_t>(gb << 5) | gc;
+    fns[4 * f + 0] = static_cast<std::uint32_t>(tb);
+    fns[4 * f + 1] = gc | (el2 << 5) | (xq << 8);
+    fns[4 * f + 2] = record(f, 0) | (static_cast<std::uint32_t>(record(f, 1)) << 16);
+    fns[4 * f + 3] = record(f, 2) | (static_cast<std::uint32_t>(record(f, 3)) << 16);
   }
+  if (grec.empty()) grec.assign(4, 0);
 
   // ---- group alias cells
   std::vector<double> acut(v.alias_cut, v.alias_cut + v.n_alias);
@@ -201,31 +216,9 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
     }
   }
 
-  // ---- lane buckets: contiguous group ranges balanced by a static cost; a
-  // range that starts inside the alias region starts at an alias ordinal o
-  // with (g + 1 + o) % 4 == 0, so its draws begin on a Philox block boundary
-  // for both streams (2 or 4 draws per block) and lanes refill in lockstep.
+  // ---- lane buckets (legacy layout field; the round-robin kernel does not use them)
   std::vector<std::uint32_t> buckets(lpt + 1, 0), aord(lpt, 0);
-  {
-    std::vector<std::uint64_t> prefix(v.n_groups + 1, 0);
-    std::vector<std::uint32_t> ord(v.n_groups + 1, 0);
-    for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
-      prefix[gi + 1] = prefix[gi] + cost[gi];
-      ord[gi + 1] = ord[gi] + (v.grp_alias_size[gi] ? 1 : 0);
-    }
-    const std::uint64_t total = prefix[v.n_groups];
-    std::uint32_t b = 0;
-    for (std::uint32_t r = 1; r < lpt; ++r) {
-      const std::uint64_t target = total * r / lpt;
-      while (b < v.n_groups && prefix[b] < target) ++b;
-      // align to a block boundary while inside the alias region
-      while (b < v.n_groups && v.grp_alias_size[b] != 0 && ((v.pert_groups + 1 + ord[b]) % 4) != 0)
-        ++b;
-      buckets[r] = std::max(b, buckets[r - 1]);
-    }
-    buckets[lpt] = v.n_groups;
-    for (std::uint32_t r = 0; r < lpt; ++r) aord[r] = ord[buckets[r]];
-  }
+  buckets[lpt] = v.n_groups;
 
   // ---- assemble
   std::size_t off = 0;
