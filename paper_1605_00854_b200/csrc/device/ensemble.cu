@@ -4,23 +4,22 @@
 // simulate(), engine.hpp:371-384), bit-exact on the injected Philox stream.
 //
 // Work decomposition: one trajectory per sub-warp of LPT lanes (LPT = 32:
-// one per warp; LPT = 1: one per thread). Lane r of a sub-warp
-//   * draws Philox blocks r, r+LPT, ... of the step's first g+1 draws (the g
-//     grouped-perturbation draws and the leaf draw) and XORs any flip into the
-//     state (engine.hpp:257-266);
-//   * a sub-warp ballot implements the short-circuit: any kept flip ends the
-//     step (engine.hpp:267); otherwise the leaf draw decides (engine.hpp:268);
-//   * in the function phase lane r owns a contiguous range of node groups
-//     (host-balanced buckets): per group one alias draw (engine.hpp:284-291),
-//     a gather of the chosen combined function's parent bits from the shared
-//     state (engine.hpp:292-302), one table lookup (engine.hpp:303) and an OR
-//     into the next state (engine.hpp:304-309), accumulated in a 96-bit
-//     register window and flushed with shared-memory atomics at word changes.
-// The plan (perturbation cells, group/function records, gather records,
-// alias cells and — when they fit — the truth tables) is staged once per CTA
-// into shared memory with one bulk copy (cp.async.bulk + mbarrier). States
-// live in shared memory (two buffers per trajectory). Statistics stay in
-// registers and are written once at the end.
+// one per warp; LPT = 1: one per thread). Per step, lane r of a sub-warp
+//   * phase A: draws Philox blocks r, r+LPT, ... holding the step's first g+1
+//     draws (the g grouped-perturbation draws and the leaf draw), looks each
+//     pattern up in the perturbation cells and XORs any flip into the state
+//     (engine.hpp:257-266); a sub-warp ballot is the short-circuit — any kept
+//     flip ends the step (engine.hpp:267), otherwise the leaf draw decides
+//     (engine.hpp:268);
+//   * function phase, in lockstep rounds: in round t lane r evaluates group
+//     t*LPT + r — one combined-function draw (engine.hpp:284-291), a gather
+//     of that function's parent bits from the shared state (engine.hpp:
+//     292-302), one table lookup (engine.hpp:303) — and the round's outputs
+//     are ORed into the next state (engine.hpp:304-309): one ballot word when
+//     every group of the round is a single node, shared-memory atomics
+//     otherwise. Phase-B draws are produced LPT blocks at a time (lane r
+//     computes one block into a per-trajectory draw buffer), because the
+//     stream starts phase B on a fresh Philox block.
 #include <cuda_runtime.h>
 
 #include <cstdint>
