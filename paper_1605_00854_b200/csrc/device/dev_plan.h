@@ -15,8 +15,9 @@
 //                      the A alias groups come first (grouping.hpp: multi-function
 //                      groups precede single-function ones), so the function phase
 //                      runs an alias region [0, A) and a plain region [A, G).
-//   fns[F]        uint4 {table byte offset,
-//                        gather count | entry log2 << 5 | extra-record quad << 8,
+//   fns[F]        uint4 {table byte offset — or, when the whole table fits in 32
+//                        bits (members * 2^gather_count <= 32), the table itself,
+//                        gather count | entry log2 << 5 | inline << 7 | extra-record quad << 8,
 //                        records 0,1 (u16 each), records 2,3}
 //   grec[...]     u16  gather records 4.. of functions with more than 4 parents,
 //                      4-aligned per function. A record is
@@ -55,6 +56,8 @@ struct dev_plan_header {
   std::uint32_t table_bytes;  // bytes [off_tables, off_tables + table_bytes)
   std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
   std::uint32_t n_alias_groups;  // A: groups [0, A) draw a combined function
+  std::uint32_t n_single_alias;  // A1 <= A: groups [0, A1) are single nodes at offset = index,
+                                 // every function's table inline (1 bit x <= 32 entries)
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

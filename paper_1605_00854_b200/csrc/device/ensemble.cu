@@ -173,8 +173,7 @@ __global__ void __launch_bounds__(1024, 1)
   std::uint32_t* S0 = reinterpret_cast<std::uint32_t*>(smem + staged) +
                       static_cast<std::size_t>(slot) * stride;
   std::uint32_t* S1 = S0 + sw32;
-  std::uint32_t* dbuf = S0 + 2 * sw32;
-  dbuf = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(dbuf) + 15) & ~std::uintptr_t(15));
+  std::uint32_t* dbuf = S0 + 2 * sw32;  // 16-B aligned: 2*sw32 is a multiple of 4
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
     for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w];
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(1024, 1)
 
   const std::uint32_t k = h.k, g = h.g;
   const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks of phase A = draws 0..g
-  const std::uint32_t A = h.n_alias_groups, NG = h.n_groups;
+  const std::uint32_t A = h.n_alias_groups, NG = h.n_groups, A1 = h.n_single_alias;
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
   mulhilo(kPhiloxM0, traj, thi0, tlo0);
@@ -193,6 +192,42 @@ __global__ void __launch_bounds__(1024, 1)
     for (std::uint32_t i = 0; i < rp.pred.n; ++i)
       ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
     return ok;
+  };
+
+  // Combined-function choice of alias group (engine.hpp:284-291) from draw jj
+  // of the draw buffer.
+  auto alias_pick = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
+    if constexpr (STREAM == STREAM_U53) {
+      // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
+      // contraction, exactly as engine.hpp:285-290 computes it.
+      const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+      const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
+      const double xx = __dmul_rn(u, __uint2double_rn(asz));
+      std::uint32_t c = __double2uint_rz(xx);
+      if (c >= asz) c = asz - 1;
+      const double fr = __dsub_rn(xx, __uint2double_rn(c));
+      return fr < ldp<GC>(acut + ab + c) ? c : ldp<GC>(aidx + ab + c);
+    } else {
+      // x*N < 2^53 is exact, so floor and fraction are the product's halves
+      const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
+      const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
+      const uint2 cell = ldp<GC>(a32 + ab + c);
+      return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
+    }
+  };
+
+  // Gathered parent valuation of combined function record F (engine.hpp:292-302).
+  auto gather_fn = [&](const std::uint32_t* Sc, const uint4& F) -> std::uint32_t {
+    const std::uint32_t gc = F.y & 31u;
+    std::uint32_t v = gather4(Sc, F.z, F.w, 0);
+    if (gc > 4) {
+      const std::uint32_t xq = F.y >> 8;
+      for (std::uint32_t q = 4; q < gc; q += 4) {
+        const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+        v |= gather4(Sc, rr.x, rr.y, q);
+      }
+    }
+    return v;
   };
 
   // One group of the function phase (engine.hpp:281-310): combined-function
@@ -205,38 +240,16 @@ __global__ void __launch_bounds__(1024, 1)
     const std::uint32_t asz = G.w & 0x7FFFFFu;
     members = (G.w >> 24) + 1;
     off = G.x;
-    std::uint32_t idx = 0;
-    if (asz != 0) {
-      if constexpr (STREAM == STREAM_U53) {
-        // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
-        // contraction, exactly as engine.hpp:285-290 computes it.
-        const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
-        const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
-        const double xx = __dmul_rn(u, __uint2double_rn(asz));
-        std::uint32_t c = __double2uint_rz(xx);
-        if (c >= asz) c = asz - 1;
-        const double fr = __dsub_rn(xx, __uint2double_rn(c));
-        idx = fr < ldp<GC>(acut + G.z + c) ? c : ldp<GC>(aidx + G.z + c);
-      } else {
-        // x*N < 2^53 is exact, so floor and fraction are the product's halves
-        const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
-        const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
-        const uint2 cell = ldp<GC>(a32 + G.z + c);
-        idx = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
-      }
-    }
+    const std::uint32_t idx = asz != 0 ? alias_pick(asz, G.z, jj) : 0u;
     const uint4 F = ldp<GC>(fns + G.y + idx);
-    const std::uint32_t gc = F.y & 31u;
-    std::uint32_t v = gather4(Sc, F.z, F.w, 0);
-    if (gc > 4) {
-      const std::uint32_t xq = F.y >> 8;
-      for (std::uint32_t q = 4; q < gc; q += 4) {
-        const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
-        v |= gather4(Sc, rr.x, rr.y, q);
-      }
+    const std::uint32_t v = gather_fn(Sc, F);
+    ohi = 0;
+    if (F.y & 0x80u) {  // inline table
+      const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
+      olo = (F.x >> (v * members)) & m;
+      return;
     }
     const std::uint32_t el2 = (F.y >> 5) & 3u;
-    ohi = 0;
     if (el2 == 0) {
       olo = ldp<GT>(tab + F.x + v);
     } else if (el2 == 1) {
@@ -334,10 +347,29 @@ __global__ void __launch_bounds__(1024, 1)
           const std::uint32_t jr = j0 + t * LPT;
           if (jr >= A) break;
           const std::uint32_t j = jr + r;
-          const bool act = j < A;
-          std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
-          if (act) eval_group(Sc, j, t * LPT + r, olo, ohi, off, members);
-          emit_round(Sn, act, olo, ohi, off, members);
+          if (jr + LPT <= A1) {
+            // single-node round: group j sits at bit j, its 1-bit table is
+            // inline in the function record; the round is one ballot word
+            const uint4 G = ldp<GC>(groups + j);
+            const uint4 F = ldp<GC>(fns + G.y + alias_pick(G.w & 0x7FFFFFu, G.z, t * LPT + r));
+            const std::uint32_t v = gather_fn(Sc, F);
+            std::uint32_t bits = __ballot_sync(smask, (F.x >> v) & 1u);
+            if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
+            if (r == 0 && bits) {
+              const std::uint32_t w = jr >> 5, sh = jr & 31;
+              if (LPT == 32) {
+                Sn[w] = bits;  // jr is a multiple of 32: the word is this round's alone
+              } else {
+                atomicOr(Sn + w, bits << sh);
+                if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
+              }
+            }
+          } else {
+            const bool act = j < A;
+            std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
+            if (act) eval_group(Sc, j, t * LPT + r, olo, ohi, off, members);
+            emit_round(Sn, act, olo, ohi, off, members);
+          }
         }
         __syncwarp(smask);
       }

@@ -155,6 +155,17 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
       fn_members[f] = members;
     }
   }
+  // leading single-node alias groups whose functions all have inline tables
+  h.n_single_alias = 0;
+  for (std::uint32_t gi = 0; gi < h.n_alias_groups; ++gi) {
+    const std::uint32_t members = (groups[4 * gi + 3] >> 24) + 1;
+    if (members != 1 || groups[4 * gi] != gi) break;
+    bool ok = true;
+    for (std::uint32_t j = 0; j < v.grp_alias_size[gi]; ++j)
+      ok = ok && v.fn_gather_count[v.grp_fn_begin[gi] + j] <= 5;
+    if (!ok) break;
+    h.n_single_alias = gi + 1;
+  }
   auto record = [&](std::uint32_t f, std::uint32_t b) -> std::uint16_t {
     const std::uint32_t gc = v.fn_gather_count[f];
     const std::uint32_t pos = b < gc ? v.fn_gather[v.fn_gather_begin[f] + b] : n;
@@ -189,8 +200,17 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
       const std::uint32_t slots = (gc + 3) & ~3u;
       for (std::uint32_t b = 4; b < slots; ++b) grec.push_back(record(f, b));
     }
-    fns[4 * f + 0] = static_cast<std::uint32_t>(tb);
-    fns[4 * f + 1] = gc | (el2 << 5) | (xq << 8);
+    // tables of at most 32 bits live inline in the record (entry e at bits
+    // [e*members, (e+1)*members))
+    std::uint32_t inl = 0, word = static_cast<std::uint32_t>(tb);
+    if (static_cast<std::uint64_t>(members) << gc <= 32) {
+      inl = 1;
+      word = 0;
+      for (std::uint64_t e = 0; e < len; ++e)
+        word |= static_cast<std::uint32_t>(v.fn_tables[v.fn_table_begin[f] + e]) << (e * members);
+    }
+    fns[4 * f + 0] = word;
+    fns[4 * f + 1] = gc | (el2 << 5) | (inl << 7) | (xq << 8);
     fns[4 * f + 2] = record(f, 0) | (static_cast<std::uint32_t>(record(f, 1)) << 16);
     fns[4 * f + 3] = record(f, 2) | (static_cast<std::uint32_t>(record(f, 3)) << 16);
   }
