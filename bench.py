@@ -219,7 +219,9 @@ def run_ours(a):
     stream = pb.STREAM_U53 if a.stream == "u53" else pb.STREAM_U32
     eng = pb.GpuEnsemble(plan, device=local, lanes_per_traj=a.lpt, placement=a.placement)
     words = eng.words
-    traj_begin = rank * n_traj
+    from paper_1605_00854_b200.ensemble import allreduce_totals, pooled, shard_range
+
+    traj_begin, _ = shard_range(n_traj * world, world, rank)  # weak scaling: n_traj per GPU
 
     states = torch.zeros((n_traj, words), dtype=torch.int64, device=dev)
     counts = torch.zeros((n_traj, 8), dtype=torch.int64, device=dev)
@@ -260,14 +262,14 @@ def run_ours(a):
         dist.barrier()
     my_ms = sum(ev_ms)
     t_ms = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    tot = torch.tensor([fn_steps], dtype=torch.int64, device=dev)
     if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-        # the single collective of the path: one all-reduce of the counts
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)  # measurement: max over ranks
     total_ms = float(t_ms.item())
-    fn_total = int(tot.item())
+    # the single collective of the path: one all-reduce of the pooled counts
+    local = pooled(counts.cpu().numpy().view(np.uint64))
+    local[6] = fn_steps  # function-phase steps over all timed launches
+    totals = allreduce_totals(local, device=dev)
+    fn_total = int(totals[6])
     traj_steps = n_traj * world * sim_steps * a.steps
     value = traj_steps * flat.n_kept / (total_ms / 1e3)
 

@@ -224,6 +224,11 @@ int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pr
                  const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
                  pbn_estimate_result* out);
 
+/* ---- test hooks over host internals (grouping.hpp:50-82, alias.hpp:18-56) ---- */
+uint32_t pbn_internal_lower_bound(const uint32_t* w, uint32_t n, uint64_t theta);
+int pbn_internal_greedy_partition(const uint32_t* w, uint32_t n, uint32_t m, uint32_t* part_of);
+int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint32_t* alias);
+
 #ifdef __cplusplus
 }
 #endif

@@ -137,6 +137,10 @@ def _load():
         "pbn_gpu_destroy": (None, [P]),
         "pbn_philox_kat": (I, [C.POINTER(U32), U32, U64, C.POINTER(U32)]),
         "pbn_estimate": (I, [P, P, P, P, U32, P, P]),
+        "pbn_internal_lower_bound": (U32, [C.POINTER(U32), U32, U64]),
+        "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
+        "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
+                                         C.POINTER(U32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -342,6 +346,34 @@ def prepare(model: Model, theta=DEFAULT_THETA, k_max=DEFAULT_K, max_group_parent
     h = C.c_void_p()
     _check(lib.pbn_prepare(model._h, theta, k_max, max_group_parents, C.byref(h)))
     return PreparedSimulation(h.value, model, theta, k_max, max_group_parents)
+
+
+def lower_bound(weights, theta):
+    """grouping.hpp:50-57 (test hook)."""
+    w = np.ascontiguousarray(weights, np.uint32)
+    return int(lib.pbn_internal_lower_bound(_u32p(w), len(w), theta))
+
+
+def greedy_partition(weights, m):
+    """grouping.hpp:63-82 (test hook): list of m lists of item indices."""
+    w = np.ascontiguousarray(weights, np.uint32)
+    part = np.zeros(len(w), np.uint32)
+    _check(lib.pbn_internal_greedy_partition(_u32p(w), len(w), m, _u32p(part)))
+    out = [[] for _ in range(m)]
+    order = sorted(range(len(w)), key=lambda i: (-int(w[i]), i))
+    for i in order:  # insertion order of the greedy pass
+        out[int(part[i])].append(i)
+    return out
+
+
+def alias_build(probs):
+    """alias.hpp:18-56 (test hook): (cut-offs, aliases)."""
+    p = np.ascontiguousarray(probs, np.float64)
+    cut = np.zeros(len(p), np.float64)
+    al = np.zeros(len(p), np.uint32)
+    _check(lib.pbn_internal_alias_build(p.ctypes.data_as(C.POINTER(C.c_double)), len(p),
+                                        cut.ctypes.data_as(C.POINTER(C.c_double)), _u32p(al)))
+    return cut, al
 
 
 def device_count() -> int:

@@ -457,6 +457,27 @@ int pbn_philox_kat(const uint32_t* ctr, uint32_t n, uint64_t seed, uint32_t* out
   });
 }
 
+// ---- test hooks over host internals -----------------------------------------
+uint32_t pbn_internal_lower_bound(const uint32_t* w, uint32_t n, uint64_t theta) {
+  return partition_lower_bound(std::vector<std::uint32_t>(w, w + n), theta);
+}
+
+int pbn_internal_greedy_partition(const uint32_t* w, uint32_t n, uint32_t m, uint32_t* part_of) {
+  return guard([&] {
+    const auto parts = greedy_product_partition(std::vector<std::uint32_t>(w, w + n), m);
+    for (uint32_t j = 0; j < parts.size(); ++j)
+      for (auto idx : parts[j]) part_of[idx] = j;
+  });
+}
+
+int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint32_t* alias) {
+  return guard([&] {
+    const walker_table t = build_walker(probs, n);
+    std::copy(t.cut.begin(), t.cut.end(), cut);
+    std::copy(t.alias.begin(), t.alias.end(), alias);
+  });
+}
+
 int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pred_bits,
                  const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
                  pbn_estimate_result* out) {

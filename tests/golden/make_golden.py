@@ -1,0 +1,65 @@
+#!/usr/bin/env python3
+"""Regenerates tests/golden/*.npz from the UNMODIFIED reference library
+(oracle/_ref/libpbnref.so, built from /root/reference/proj/include by
+oracle/Makefile). Run in the development container (needs /root/reference to
+build _ref); the fixtures are committed and travel to the GPU box.
+
+Each fixture: the BASELINE-shaped model text (sha256), the reference plan's
+digest, and pbn::simulate(grouped_simulator) results on the injected Philox
+stream for a few trajectories (both stream kinds, predicate on, nonzero
+traj_begin/step_begin)."""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import oracle  # noqa: E402
+from helpers import config_text, flat_of, plan_digest  # noqa: E402
+
+FIXTURES = {
+    # name: (config, k_max, mgp, n_traj, n_steps)
+    "c1": ("c1", 12, 8, 8, 600),
+    "c2": ("c2", 12, 8, 4, 200),
+    "c3": ("c3", 12, 8, 8, 600),
+    "c4": ("c4", 12, 12, 2, 60),
+    "c5": ("c5", 12, 8, 4, 200),
+}
+SEED, TRAJ_BEGIN, STEP_BEGIN = 42, 1000, 7
+
+
+def main():
+    ref = oracle.Reference()
+    manifest = {}
+    for name, (cfg, k, mgp, n_traj, n_steps) in FIXTURES.items():
+        text, terms = config_text(cfg)
+        rplan = ref.parse(text).prepare(1 << 25, k, mgp)
+        pred = rplan.compile_predicate(terms)
+        out = {}
+        for stream in (0, 1):
+            st, cnt = rplan.simulate_philox(SEED, TRAJ_BEGIN, n_traj, n_steps, pred=pred,
+                                            stream=stream, step_begin=STEP_BEGIN)
+            out[f"states_s{stream}"] = st
+            out[f"counts_s{stream}"] = cnt
+        out["pred_bits"], out["pred_vals"] = pred
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+        manifest[name] = {
+            "config": cfg, "k_max": k, "mgp": mgp, "theta": 1 << 25, "n_traj": n_traj,
+            "n_steps": n_steps, "seed": SEED, "traj_begin": TRAJ_BEGIN, "step_begin": STEP_BEGIN,
+            "model_sha256": hashlib.sha256(text.encode()).hexdigest(),
+            "plan_digest": plan_digest(flat_of(rplan.view)), "n_kept": rplan.n_kept,
+            "terms": terms,
+        }
+        print(name, manifest[name]["n_kept"], manifest[name]["plan_digest"][:16], flush=True)
+    with open(os.path.join(HERE, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
