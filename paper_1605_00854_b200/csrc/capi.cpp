@@ -20,7 +20,7 @@
 
 namespace pbn_b200 {
 cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
-                            int stream_kind, std::uint32_t warps_per_cta,
+                            int stream_kind, std::uint32_t lpt, std::uint32_t warps_per_cta,
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches);
@@ -54,6 +54,8 @@ struct pbn_gpu {
   std::size_t cap_traj = 0;
   std::uint32_t launches = 0;
   std::uint32_t last_warps = 0;
+  std::uint32_t lpt_fixed = 0;  // 0: chosen per run
+  std::uint32_t last_lpt = 0;
 };
 
 namespace {
@@ -93,11 +95,12 @@ void need(const void* p, const char* what) {
 
 constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory states
 
-std::uint32_t auto_lpt(std::uint32_t n_kept) {
-  if (n_kept <= 96) return 4;
-  if (n_kept <= 256) return 8;
-  if (n_kept <= 512) return 16;
-  return 32;
+// Lanes per trajectory: by network size, then doubled until the ensemble
+// gives ~24 resident warps per SM (latency hiding) or one warp per trajectory.
+std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t sms) {
+  std::uint32_t lpt = n_kept <= 96 ? 4 : n_kept <= 256 ? 8 : n_kept <= 512 ? 16 : 32;
+  while (lpt < 32 && n_traj * lpt / 32 < static_cast<std::uint64_t>(sms) * 24) lpt *= 2;
+  return lpt;
 }
 
 std::uint32_t staged_bytes(const pbn_gpu& g) {
@@ -108,8 +111,7 @@ std::uint32_t staged_bytes(const pbn_gpu& g) {
 
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
-std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj) {
-  const std::uint32_t lpt = g.ep.h.lpt;
+std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt) {
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(32, w));
@@ -149,10 +151,11 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
   const dev_run_params rp = make_params(g, a);
   if (a.n_traj == 0) return;
   ck(cudaSetDevice(g.device), "cudaSetDevice");
-  g.last_warps = pick_warps(g, a.n_traj);
+  g.last_lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
+  g.last_warps = pick_warps(g, a.n_traj, g.last_lpt);
   g.launches = 0;
-  ck(launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_warps, rp,
-                     d_states, d_counts, stream, &g.launches),
+  ck(launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_lpt,
+                     g.last_warps, rp, d_states, d_counts, stream, &g.launches),
      "ensemble launch");
 }
 
@@ -341,7 +344,10 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
     need(out, "out");
     auto g = std::make_unique<pbn_gpu>();
     g->device = device;
-    g->ep = encode_plan(*view, lpt ? lpt : auto_lpt(view->n_kept));
+    if (lpt != 0 && (lpt > 32 || (lpt & (lpt - 1)) != 0))
+      throw std::invalid_argument("lanes per trajectory must be 0 (auto) or a power of two <= 32");
+    g->lpt_fixed = lpt;
+    g->ep = encode_plan(*view);
     ck(cudaSetDevice(device), "cudaSetDevice");
     int optin = 0, sms = 0;
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
@@ -382,7 +388,7 @@ int pbn_gpu_info(const pbn_gpu* g, uint32_t* lpt, uint32_t* tables_in_smem, uint
                  uint64_t* plan_bytes, uint32_t* warps_per_cta) {
   return guard([&] {
     need(g, "gpu");
-    if (lpt) *lpt = g->ep.h.lpt;
+    if (lpt) *lpt = g->last_lpt ? g->last_lpt : g->lpt_fixed;
     if (tables_in_smem) *tables_in_smem = static_cast<uint32_t>(g->place);
     if (smem_bytes) *smem_bytes = staged_bytes(*g);
     if (plan_bytes) *plan_bytes = g->ep.blob.size();

@@ -27,8 +27,8 @@
 //   acut[A]       f64  group alias cut-offs (U53 path, FP64 like engine.hpp:285-290)
 //   aidx[A]       u32  group alias targets
 //   a32[A]        uint2 {ceil(cut * 2^32) or 0, alias or self}: U32 integer path
-//   buckets[L+1]  u32  group range of lane r: [buckets[r], buckets[r+1])
-//   aord[L]       u32  alias ordinal of the first alias group in lane r's range
+//   arec[A1]      u32  compact record of the leading single-node alias groups:
+//                      base | alias_size << 24 (their fn_begin == alias_begin == base)
 //   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
 #pragma once
 
@@ -45,19 +45,19 @@ struct dev_plan_header {
   std::uint32_t k;          // perturbation width
   std::uint32_t last_mask;  // 2^k' - 1 (k' <= 24)
   std::uint32_t n_groups;
-  std::uint32_t lpt;        // lanes per trajectory the buckets were cut for
   std::uint32_t max_alias;  // largest group alias table
   std::uint64_t leaf_thr53; // floor(t * 2^53): leaf perturbation iff r53 > thr
   std::uint32_t leaf_thr32; // floor(t * 2^32) (saturated)
   std::uint32_t leaf_never; // t == 1: the leaf draw can never fire
   std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
-  std::uint32_t off_acut, off_aidx, off_a32, off_buckets, off_aord, off_tables;
+  std::uint32_t off_acut, off_aidx, off_a32, off_arec, off_tables;
   std::uint32_t core_bytes;   // bytes [0, off_tables)
   std::uint32_t table_bytes;  // bytes [off_tables, off_tables + table_bytes)
   std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
   std::uint32_t n_alias_groups;  // A: groups [0, A) draw a combined function
   std::uint32_t n_single_alias;  // A1 <= A: groups [0, A1) are single nodes at offset = index,
                                  // every function's table inline (1 bit x <= 32 entries)
+  std::uint32_t rg_ok;           // sw32 <= 32: one state word per lane fits a warp (SHFL gather)
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

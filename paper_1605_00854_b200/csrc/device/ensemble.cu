@@ -129,7 +129,22 @@ __device__ __forceinline__ std::uint32_t gather4(const std::uint32_t* S, std::ui
          (__funnelshift_r(w2, w2, r2) & (4u << b0)) | (__funnelshift_r(w3, w3, r3) & (8u << b0));
 }
 
-template <int LPT, int STREAM, int PLACE>
+// Same, with the state held one word per lane (n' <= 1023, LPT = 32): the
+// parent word comes from a shuffle (the source lane index is taken mod 32, so
+// the packed record needs no masking) instead of a shared-memory load.
+__device__ __forceinline__ std::uint32_t gather4_shfl(std::uint32_t wreg, std::uint32_t p01,
+                                                      std::uint32_t p23, std::uint32_t b0) {
+  const std::uint32_t w0 = __shfl_sync(0xFFFFFFFFu, wreg, p01 >> 5);
+  const std::uint32_t w1 = __shfl_sync(0xFFFFFFFFu, wreg, p01 >> 21);
+  const std::uint32_t w2 = __shfl_sync(0xFFFFFFFFu, wreg, p23 >> 5);
+  const std::uint32_t w3 = __shfl_sync(0xFFFFFFFFu, wreg, p23 >> 21);
+  return (__funnelshift_r(w0, w0, p01) & (1u << b0)) |
+         (__funnelshift_r(w1, w1, p01 >> 16) & (2u << b0)) |
+         (__funnelshift_r(w2, w2, p23) & (4u << b0)) |
+         (__funnelshift_r(w3, w3, p23 >> 16) & (8u << b0));
+}
+
+template <int LPT, int STREAM, int PLACE, bool RG>
 __global__ void __launch_bounds__(1024, 1)
     pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                         const dev_run_params rp, std::uint64_t* __restrict__ states,
@@ -155,6 +170,7 @@ __global__ void __launch_bounds__(1024, 1)
   const double* acut = reinterpret_cast<const double*>(core + h.off_acut);
   const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(core + h.off_aidx);
   const uint2* a32 = reinterpret_cast<const uint2*>(core + h.off_a32);
+  const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
 
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t r = lane % LPT;
@@ -189,7 +205,10 @@ __global__ void __launch_bounds__(1024, 1)
 
   auto pred_eval = [&](const std::uint32_t* S) -> std::uint32_t {
     std::uint32_t ok = rp.pred.n ? 1u : 0u;
-    for (std::uint32_t i = 0; i < rp.pred.n; ++i)
+#pragma unroll
+    for (std::uint32_t i = 0; i < 4; ++i)
+      if (i < rp.pred.n) ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
+    for (std::uint32_t i = 4; i < rp.pred.n; ++i)
       ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
     return ok;
   };
@@ -287,6 +306,12 @@ __global__ void __launch_bounds__(1024, 1)
     }
   };
 
+  // gather records of slots 4..7 pointing at the always-zero bit n'
+  auto zrec = [&](std::uint32_t b) -> std::uint32_t {
+    return ((h.n_kept >> 5) << 5) | (((h.n_kept & 31) - b) & 31);
+  };
+  const std::uint32_t zrec01 = zrec(4) | (zrec(5) << 16), zrec23 = zrec(6) | (zrec(7) << 16);
+
   std::uint32_t cur = 0;
   std::uint32_t prev = pred_eval(S0);
   std::uint32_t n01 = 0, n10 = 0, n11 = 0, nfn = 0, npert = 0;
@@ -334,6 +359,8 @@ __global__ void __launch_bounds__(1024, 1)
       // ---- function phase, in lockstep rounds of LPT groups
       std::uint32_t* Sn = cur ? S0 : S1;
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
+      std::uint32_t wreg = 0;  // RG: state word `lane` of the current state
+      if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
       // alias region: chunks of LPT*DPB draws; lane r first computes phase-B
       // block nb0 + j0/DPB + r into the draw buffer
       for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB) {
@@ -350,9 +377,23 @@ __global__ void __launch_bounds__(1024, 1)
           if (jr + LPT <= A1) {
             // single-node round: group j sits at bit j, its 1-bit table is
             // inline in the function record; the round is one ballot word
-            const uint4 G = ldp<GC>(groups + j);
-            const uint4 F = ldp<GC>(fns + G.y + alias_pick(G.w & 0x7FFFFFu, G.z, t * LPT + r));
-            const std::uint32_t v = gather_fn(Sc, F);
+            const std::uint32_t ar = ldp<GC>(arec + j);
+            const std::uint32_t base = ar & 0xFFFFFFu;
+            const uint4 F = ldp<GC>(fns + base + alias_pick(ar >> 24, base, t * LPT + r));
+            std::uint32_t v;
+            if constexpr (RG) {
+              // shuffles need the whole warp: the 5th parent (if any lane has
+              // one) is gathered by every lane, others read the zero bit n'
+              v = gather4_shfl(wreg, F.z, F.w, 0);
+              const bool more = (F.y & 31u) > 4;
+              if (__any_sync(0xFFFFFFFFu, more)) {
+                uint2 rr = make_uint2(zrec01, zrec23);
+                if (more) rr = ldp<GC>(grec + (F.y >> 8));
+                v |= gather4_shfl(wreg, rr.x, rr.y, 4);
+              }
+            } else {
+              v = gather_fn(Sc, F);
+            }
             std::uint32_t bits = __ballot_sync(smask, (F.x >> v) & 1u);
             if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
             if (r == 0 && bits) {
@@ -428,55 +469,59 @@ __global__ void pbn_philox_kat_kernel(const uint4* ctr, std::uint32_t k0, std::u
 using kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
                            std::uint64_t*, std::uint64_t*);
 
-template <int LPT, int STREAM>
+template <int LPT, int STREAM, bool RG>
 kernel_fn pick_place(int place) {
   switch (place) {
     case PLACE_ALL:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, RG>;
     case PLACE_CORE:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, RG>;
     default:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL, RG>;
   }
 }
 
 template <int STREAM>
-kernel_fn pick_lpt(std::uint32_t lpt, int place) {
+kernel_fn pick_lpt(std::uint32_t lpt, int place, bool rg) {
   switch (lpt) {
     case 1:
-      return pick_place<1, STREAM>(place);
+      return pick_place<1, STREAM, false>(place);
     case 2:
-      return pick_place<2, STREAM>(place);
+      return pick_place<2, STREAM, false>(place);
     case 4:
-      return pick_place<4, STREAM>(place);
+      return pick_place<4, STREAM, false>(place);
     case 8:
-      return pick_place<8, STREAM>(place);
+      return pick_place<8, STREAM, false>(place);
     case 16:
-      return pick_place<16, STREAM>(place);
+      return pick_place<16, STREAM, false>(place);
     default:
-      return pick_place<32, STREAM>(place);
+      return rg ? pick_place<32, STREAM, true>(place) : pick_place<32, STREAM, false>(place);
   }
 }
 
-kernel_fn select_kernel(std::uint32_t lpt, int stream, int place) {
-  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place)
-                              : pick_lpt<STREAM_U32>(lpt, place);
+kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, bool rg) {
+  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, rg)
+                              : pick_lpt<STREAM_U32>(lpt, place, rg);
+}
+
+std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt) {
+  return (2 * h.sw32 + lpt * 4 + 3) & ~3u;
 }
 
 cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
-                            int stream_kind, std::uint32_t warps_per_cta,
+                            int stream_kind, std::uint32_t lpt, std::uint32_t warps_per_cta,
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches) {
-  const kernel_fn fn = select_kernel(h.lpt, stream_kind, place);
+  const bool rg = lpt == 32 && h.rg_ok && h.n_single_alias >= 32;
+  const kernel_fn fn = select_kernel(lpt, stream_kind, place, rg);
   const std::uint32_t threads = warps_per_cta * 32;
-  const std::uint32_t slots = threads / h.lpt;
+  const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;
   std::size_t staged = 0;
   if (place == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
   if (place == PLACE_CORE) staged = h.core_bytes;
-  const std::size_t stride = (2 * h.sw32 + h.lpt * 4 + 3) & ~3u;
-  const std::size_t smem = staged + static_cast<std::size_t>(slots) * stride * 4 + 16;
+  const std::size_t smem = staged + static_cast<std::size_t>(slots) * slot_words(h, lpt) * 4 + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

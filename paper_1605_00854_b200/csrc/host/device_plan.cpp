@@ -66,9 +66,7 @@ dev_predicate compile_dev_predicate(const std::uint32_t* bits, const std::uint8_
   return p;
 }
 
-encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
-  if (lpt == 0 || lpt > 32 || (lpt & (lpt - 1)) != 0)
-    throw model_error("lanes per trajectory must be a power of two in [1, 32]");
+encoded_plan encode_plan(const pbn_plan_view& v) {
   const std::uint32_t n = v.n_kept;
   if (n == 0) throw model_error("empty plan");
   if (n >= 65535) throw resource_error("device engine supports at most 65534 kept nodes");
@@ -83,7 +81,7 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
   h.k = v.pert_k;
   h.last_mask = static_cast<std::uint32_t>(v.pert_mask);
   h.n_groups = v.n_groups;
-  h.lpt = lpt;
+  h.rg_ok = h.sw32 <= 32 ? 1u : 0u;
   // leaf perturbation iff u > t  <=>  r > floor(t * 2^bits) (t*2^bits is exact)
   const double t53 = std::floor(std::ldexp(v.t, 53));
   h.leaf_thr53 = static_cast<std::uint64_t>(t53);
@@ -157,15 +155,21 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
   }
   // leading single-node alias groups whose functions all have inline tables
   h.n_single_alias = 0;
+  std::vector<std::uint32_t> arec;
   for (std::uint32_t gi = 0; gi < h.n_alias_groups; ++gi) {
     const std::uint32_t members = (groups[4 * gi + 3] >> 24) + 1;
     if (members != 1 || groups[4 * gi] != gi) break;
+    if (v.grp_fn_begin[gi] != v.grp_alias_begin[gi] || v.grp_alias_size[gi] > 255 ||
+        v.grp_fn_begin[gi] >= (1u << 24))
+      break;
     bool ok = true;
     for (std::uint32_t j = 0; j < v.grp_alias_size[gi]; ++j)
       ok = ok && v.fn_gather_count[v.grp_fn_begin[gi] + j] <= 5;
     if (!ok) break;
     h.n_single_alias = gi + 1;
+    arec.push_back(v.grp_fn_begin[gi] | (v.grp_alias_size[gi] << 24));
   }
+  if (arec.empty()) arec.push_back(0);
   auto record = [&](std::uint32_t f, std::uint32_t b) -> std::uint16_t {
     const std::uint32_t gc = v.fn_gather_count[f];
     const std::uint32_t pos = b < gc ? v.fn_gather[v.fn_gather_begin[f] + b] : n;
@@ -236,10 +240,6 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
     }
   }
 
-  // ---- lane buckets (legacy layout field; the round-robin kernel does not use them)
-  std::vector<std::uint32_t> buckets(lpt + 1, 0), aord(lpt, 0);
-  buckets[lpt] = v.n_groups;
-
   // ---- assemble
   std::size_t off = 0;
   auto section = [&](std::size_t bytes) {
@@ -255,8 +255,7 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
   h.off_acut = section(8 * acut.size());
   h.off_aidx = section(4 * aidx.size());
   h.off_a32 = section(4 * a32.size());
-  h.off_buckets = section(4 * buckets.size());
-  h.off_aord = section(4 * aord.size());
+  h.off_arec = section(4 * arec.size());
   h.core_bytes = static_cast<std::uint32_t>(off);
   h.off_tables = static_cast<std::uint32_t>(off);
   h.table_bytes = static_cast<std::uint32_t>(align16(tables.size()));
@@ -270,8 +269,7 @@ encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt) {
   put(ep.blob, h.off_acut, acut);
   put(ep.blob, h.off_aidx, aidx);
   put(ep.blob, h.off_a32, a32);
-  put(ep.blob, h.off_buckets, buckets);
-  put(ep.blob, h.off_aord, aord);
+  put(ep.blob, h.off_arec, arec);
   put(ep.blob, h.off_tables, tables);
   return ep;
 }

@@ -15,8 +15,7 @@ struct encoded_plan {
   std::vector<std::uint8_t> blob;  // core sections then tables
 };
 
-// lpt: lanes per trajectory (1..32, power of two) the group buckets are cut for.
-encoded_plan encode_plan(const pbn_plan_view& v, std::uint32_t lpt);
+encoded_plan encode_plan(const pbn_plan_view& v);
 
 // Predicate terms (engine bit, value) -> per-word masks (engine.hpp:328-332).
 dev_predicate compile_dev_predicate(const std::uint32_t* bits, const std::uint8_t* vals,

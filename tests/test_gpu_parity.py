@@ -18,6 +18,9 @@ CASES = {
     "c5": (2000, (1, 3), (1, 4), 0.01, 0.0, 2, False, 1609, 12, 8),
     "c1_k16": (100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 16, 12),
     "tiny": (6, (1, 3), (1, 3), 0.25, 0.0, 2, False, 7, 3, 18),
+    # n' <= 1023 with 5-parent functions: exercises the register/shuffle gather's 5th slot
+    "p5": (900, (1, 4), (1, 5), 0.002, 0.0, 2, False, 11, 12, 8),
+    "c4": (5000, (1, 4), (1, 5), 0.0001, 0.0, 2, False, 1608, 12, 12),
 }
 
 
@@ -33,11 +36,13 @@ def cuda_ok(pb):
     assert pb.device_count() >= 1, "no CUDA device visible"
 
 
-@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16"])
+@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16", "p5", "c4"])
 @pytest.mark.parametrize("stream", [0, 1])
 def test_bit_exact_vs_oracle(pb, orc, cuda_ok, case, stream):
     plan, pred = _setup(pb, case)
     n_traj, n_steps = (96, 400) if plan.n_kept > 500 else (256, 2000)
+    if plan.n_kept > 3000:
+        n_traj, n_steps = 40, 150
     eng = pb.GpuEnsemble(plan)
     st, cnt = eng.simulate(seed=42, n_traj=n_traj, n_steps=n_steps, pred=pred, stream=stream)
     ost, ocnt = orc.simulate(plan.view, 42, 0, n_traj, n_steps, pred=pred, stream=stream)
