@@ -58,6 +58,7 @@ struct dev_plan_header {
   std::uint32_t n_single_alias;  // A1 <= A: groups [0, A1) are single nodes at offset = index,
                                  // every function's table inline (1 bit x <= 32 entries)
   std::uint32_t rg_ok;           // sw32 <= 32: one state word per lane fits a warp (SHFL gather)
+  std::uint32_t single_gc5;      // some function of groups [0, A1) has 5 parents
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

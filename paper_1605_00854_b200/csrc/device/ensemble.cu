@@ -312,6 +312,40 @@ __global__ void __launch_bounds__(1024, 1)
   };
   const std::uint32_t zrec01 = zrec(4) | (zrec(5) << 16), zrec23 = zrec(6) | (zrec(7) << 16);
 
+  // Output bit of single-node alias group j (offset j, inline 1-bit table):
+  // loads and shuffles only, so two calls can be interleaved by the scheduler.
+  auto single_bit = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t j,
+                        std::uint32_t jj) -> std::uint32_t {
+    const std::uint32_t ar = ldp<GC>(arec + j);
+    const std::uint32_t base = ar & 0xFFFFFFu;
+    const uint4 F = ldp<GC>(fns + base + alias_pick(ar >> 24, base, jj));
+    std::uint32_t v;
+    if constexpr (RG) {
+      v = gather4_shfl(wreg, F.z, F.w, 0);
+      if (h.single_gc5) {  // plan-uniform: every lane takes the same branch
+        uint2 rr = make_uint2(zrec01, zrec23);
+        if ((F.y & 31u) > 4) rr = ldp<GC>(grec + (F.y >> 8));
+        v |= gather4_shfl(wreg, rr.x, rr.y, 4);
+      }
+    } else {
+      v = gather_fn(Sc, F);
+    }
+    return (F.x >> v) & 1u;
+  };
+  // A single-node round's ballot word lands at bit jr of the next state.
+  auto store_bits = [&](std::uint32_t* Sn, std::uint32_t jr, std::uint32_t bits) {
+    if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
+    if (r == 0 && bits) {
+      const std::uint32_t w = jr >> 5, sh = jr & 31;
+      if (LPT == 32) {
+        Sn[w] = bits;  // jr is a multiple of 32: the word is this round's alone
+      } else {
+        atomicOr(Sn + w, bits << sh);
+        if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
+      }
+    }
+  };
+
   std::uint32_t cur = 0;
   std::uint32_t prev = pred_eval(S0);
   std::uint32_t n01 = 0, n10 = 0, n11 = 0, nfn = 0, npert = 0;
@@ -369,47 +403,32 @@ __global__ void __launch_bounds__(1024, 1)
           *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
         }
         __syncwarp(smask);
+        // rounds are taken in pairs: both rounds' loads are issued before
+        // either ballot/store, so the two dependency chains overlap
 #pragma unroll
-        for (std::uint32_t t = 0; t < DPB; ++t) {
-          const std::uint32_t jr = j0 + t * LPT;
-          if (jr >= A) break;
-          const std::uint32_t j = jr + r;
-          if (jr + LPT <= A1) {
-            // single-node round: group j sits at bit j, its 1-bit table is
-            // inline in the function record; the round is one ballot word
-            const std::uint32_t ar = ldp<GC>(arec + j);
-            const std::uint32_t base = ar & 0xFFFFFFu;
-            const uint4 F = ldp<GC>(fns + base + alias_pick(ar >> 24, base, t * LPT + r));
-            std::uint32_t v;
-            if constexpr (RG) {
-              // shuffles need the whole warp: the 5th parent (if any lane has
-              // one) is gathered by every lane, others read the zero bit n'
-              v = gather4_shfl(wreg, F.z, F.w, 0);
-              const bool more = (F.y & 31u) > 4;
-              if (__any_sync(0xFFFFFFFFu, more)) {
-                uint2 rr = make_uint2(zrec01, zrec23);
-                if (more) rr = ldp<GC>(grec + (F.y >> 8));
-                v |= gather4_shfl(wreg, rr.x, rr.y, 4);
-              }
+        for (std::uint32_t t = 0; t < DPB; t += 2) {
+          const std::uint32_t jr0 = j0 + t * LPT, jr1 = jr0 + LPT;
+          if (jr0 >= A) break;
+          if (jr1 + LPT <= A1) {
+            const std::uint32_t b0 = single_bit(Sc, wreg, jr0 + r, t * LPT + r);
+            const std::uint32_t b1 = single_bit(Sc, wreg, jr1 + r, (t + 1) * LPT + r);
+            store_bits(Sn, jr0, __ballot_sync(smask, b0));
+            store_bits(Sn, jr1, __ballot_sync(smask, b1));
+            continue;
+          }
+#pragma unroll
+          for (std::uint32_t u = 0; u < 2; ++u) {
+            const std::uint32_t jr = jr0 + u * LPT;
+            if (jr >= A) break;
+            const std::uint32_t j = jr + r;
+            if (jr + LPT <= A1) {
+              store_bits(Sn, jr, __ballot_sync(smask, single_bit(Sc, wreg, j, (t + u) * LPT + r)));
             } else {
-              v = gather_fn(Sc, F);
+              const bool act = j < A;
+              std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
+              if (act) eval_group(Sc, j, (t + u) * LPT + r, olo, ohi, off, members);
+              emit_round(Sn, act, olo, ohi, off, members);
             }
-            std::uint32_t bits = __ballot_sync(smask, (F.x >> v) & 1u);
-            if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
-            if (r == 0 && bits) {
-              const std::uint32_t w = jr >> 5, sh = jr & 31;
-              if (LPT == 32) {
-                Sn[w] = bits;  // jr is a multiple of 32: the word is this round's alone
-              } else {
-                atomicOr(Sn + w, bits << sh);
-                if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
-              }
-            }
-          } else {
-            const bool act = j < A;
-            std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
-            if (act) eval_group(Sc, j, t * LPT + r, olo, ohi, off, members);
-            emit_round(Sn, act, olo, ohi, off, members);
           }
         }
         __syncwarp(smask);

@@ -155,6 +155,7 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   }
   // leading single-node alias groups whose functions all have inline tables
   h.n_single_alias = 0;
+  h.single_gc5 = 0;
   std::vector<std::uint32_t> arec;
   for (std::uint32_t gi = 0; gi < h.n_alias_groups; ++gi) {
     const std::uint32_t members = (groups[4 * gi + 3] >> 24) + 1;
@@ -162,10 +163,13 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     if (v.grp_fn_begin[gi] != v.grp_alias_begin[gi] || v.grp_alias_size[gi] > 255 ||
         v.grp_fn_begin[gi] >= (1u << 24))
       break;
-    bool ok = true;
-    for (std::uint32_t j = 0; j < v.grp_alias_size[gi]; ++j)
+    bool ok = true, gc5 = false;
+    for (std::uint32_t j = 0; j < v.grp_alias_size[gi]; ++j) {
       ok = ok && v.fn_gather_count[v.grp_fn_begin[gi] + j] <= 5;
+      gc5 = gc5 || v.fn_gather_count[v.grp_fn_begin[gi] + j] == 5;
+    }
     if (!ok) break;
+    if (gc5) h.single_gc5 = 1;
     h.n_single_alias = gi + 1;
     arec.push_back(v.grp_fn_begin[gi] | (v.grp_alias_size[gi] << 24));
   }
