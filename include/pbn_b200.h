@@ -138,6 +138,24 @@ typedef struct pbn_run_args {
   const uint8_t* pred_vals;   /* wanted values                                              */
   uint32_t n_pred;            /* 0 = no predicate (hits/transitions stay 0)                */
   uint32_t flags;             /* PBN_RUN_*                                                  */
+  /* Predicate-process transitions (estimator.hpp:76-102) are counted between
+   * samples taken every `kappa`-th step of the call (0 or 1: every step). The
+   * first "previous" sample is the input state's predicate with sampling
+   * phase 0 (thin_mode 0), carried over with its phase from tprev[traj] =
+   * prev | phase << 2 (1; prev 2 = none), or none (2). tprev (n_traj bytes) is
+   * updated when non-NULL. kappa <= 63. */
+  uint32_t kappa;
+  uint32_t thin_mode;
+  uint8_t* tprev;
+  /* Optional predicate series: step i -> bit series_bit0 + i of the
+   * trajectory's row of series_stride u32 words; series_init also records the
+   * input state's bit at series_bit0 - 1. (pbn_gpu_run: host pointers, copied;
+   * pbn_gpu_run_device: device pointers.) */
+  uint32_t* series;
+  uint64_t series_stride;
+  uint64_t series_bit0;
+  uint32_t series_init;
+  uint32_t reserved;
 } pbn_run_args;
 
 /* ---- errors / library info ------------------------------------------------- */
@@ -220,9 +238,32 @@ typedef struct pbn_estimate_result {
   double wall_seconds;
 } pbn_estimate_result;
 
+/* Device ensemble: req->n_traj trajectories (global ids traj_begin..), states
+ * in/out on the host (n_traj * pbn_state_words words, engine order). */
 int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pred_bits,
                  const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
                  pbn_estimate_result* out);
+
+/* The same estimator over a caller-supplied stepping backend (e.g. a CPU
+ * restatement in tests): the host logic is backend-agnostic, like the
+ * reference's estimate_steady_state<Stepper, Rng>. */
+typedef struct pbn_estimator_backend {
+  void* user;
+  uint32_t n_traj;
+  uint32_t reserved;
+  uint64_t series_capacity; /* stored pilot bits per trajectory */
+  /* advance every trajectory n_steps from step_begin; pooled counts into
+   * totals[PBN_COUNT_FIELDS]; series_bit0 == UINT64_MAX: no series. 0 = ok */
+  int (*run)(void* user, uint64_t step_begin, uint64_t n_steps, uint32_t kappa,
+             uint32_t thin_mode, uint64_t series_bit0, uint32_t series_init, uint64_t* totals);
+  /* pooled series statistics over positions [0, len): n_ijk[8], thinned pairs[4], ones */
+  int (*series_stats)(void* user, uint32_t kappa, uint64_t len, uint64_t* out13);
+} pbn_estimator_backend;
+int pbn_estimate_with_backend(const pbn_estimate_request* req, const pbn_estimator_backend* be,
+                              pbn_estimate_result* out);
+int pbn_series_stats_host(const uint32_t* series, uint32_t n_traj, uint64_t stride, uint64_t len,
+                          uint32_t kappa, uint64_t* out13);
+double pbn_inverse_normal_cdf(double p);
 
 /* ---- test hooks over host internals (grouping.hpp:50-82, alias.hpp:18-56) ---- */
 uint32_t pbn_internal_lower_bound(const uint32_t* w, uint32_t n, uint64_t theta);

@@ -76,6 +76,10 @@ class Oracle:
                                    C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32),
                                    C.POINTER(C.c_uint8), C.c_uint32, C.POINTER(C.c_uint64),
                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.orc_simulate_ex.restype = C.c_int
+        L.orc_simulate_ex.argtypes = L.orc_simulate.argtypes + [
+            C.c_uint32, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.c_uint64,
+            C.c_uint64, C.c_int]
         L.orc_step_scripted.restype = C.c_int
         L.orc_step_scripted.argtypes = [C.POINTER(PlanView), C.POINTER(C.c_uint64),
                                         C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_uint32)]
@@ -100,6 +104,27 @@ class Oracle:
                                    _u64p(counts), _u64p(nc) if nc is not None else None)
         assert rc == 0
         return (st, counts, nc) if node_counts else (st, counts)
+
+    def simulate_ex(self, view, seed, traj_begin, n_traj, n_steps, states=None, step_begin=0,
+                    pred=None, stream=0, kappa=1, thin_mode=0, tprev=None, series=None,
+                    series_bit0=0, series_init=False):
+        """orc_simulate_ex: sampled transitions (kappa/thin_mode/tprev) and an
+        optional predicate series (updated in place)."""
+        words = view.n_kept // 64 + 1
+        st = (np.zeros((n_traj, words), np.uint64) if states is None
+              else np.ascontiguousarray(states, np.uint64).copy())
+        counts = np.zeros((n_traj, 8), np.uint64)
+        bits = np.zeros(1, np.uint32) if pred is None else np.ascontiguousarray(pred[0], np.uint32)
+        vals = np.zeros(1, np.uint8) if pred is None else np.ascontiguousarray(pred[1], np.uint8)
+        npred = 0 if pred is None else len(pred[0])
+        rc = self.lib.orc_simulate_ex(
+            _as_view(view), seed, traj_begin, n_traj, stream, step_begin, n_steps, _u32p(bits),
+            _u8p(vals), npred, _u64p(st), _u64p(counts), None, kappa, thin_mode,
+            _u8p(tprev) if tprev is not None else None,
+            _u32p(series) if series is not None else None,
+            series.shape[1] if series is not None else 0, series_bit0, 1 if series_init else 0)
+        assert rc == 0
+        return st, counts
 
     def step_scripted(self, view, state_words, uniforms):
         st = np.ascontiguousarray(state_words, np.uint64).copy()

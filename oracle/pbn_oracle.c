@@ -97,27 +97,52 @@ static int orc_pred(const uint64_t* s, const uint32_t* bits, const uint8_t* vals
 
 /*
  * simulate() (engine.hpp:371-384) for a block of trajectories, with the
- * trajectory-keyed stream and the extra statistics the ensemble reports
- * (transition counts of the predicate process, step-class counts).
+ * trajectory-keyed stream and the extra statistics the ensemble reports:
+ *   - hits: steps whose post-step state satisfies the predicate (engine.hpp:380);
+ *   - transitions of the predicate process sampled every `kappa`-th step of
+ *     the call (steps i with (i+1) % kappa == 0), between consecutive samples —
+ *     the estimator's thinned_counts (estimator.hpp:76-102). thin_mode 0: the
+ *     first "previous" sample is the input state's predicate (kappa = 1 gives
+ *     the raw chain of estimator.hpp:155-170) and the sampling phase starts at
+ *     0; 1: both continue from tprev[t] = prev | phase << 2 (prev 2 = none) of
+ *     the previous call; 2: no previous sample, phase 0. tprev[t] is updated
+ *     when non-NULL;
+ *   - step classes (function phase ran / kept flip).
+ * series (optional, stride words per trajectory): predicate bit of step i at
+ * bit series_bit0 + i; if series_init, the input state's bit at series_bit0 - 1.
  * states_inout: n_traj * (n_kept/64+1) words. counts_out: n_traj * 8.
  * node_counts_out (optional): n_traj * n_kept.
  */
-int orc_simulate(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, uint32_t n_traj,
-                 int stream_kind, uint64_t step_begin, uint64_t n_steps,
-                 const uint32_t* pred_bits, const uint8_t* pred_vals, uint32_t n_pred,
-                 uint64_t* states_inout, uint64_t* counts_out, uint64_t* node_counts_out) {
+int orc_simulate_ex(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, uint32_t n_traj,
+                    int stream_kind, uint64_t step_begin, uint64_t n_steps,
+                    const uint32_t* pred_bits, const uint8_t* pred_vals, uint32_t n_pred,
+                    uint64_t* states_inout, uint64_t* counts_out, uint64_t* node_counts_out,
+                    uint32_t kappa, int thin_mode, uint8_t* tprev, uint32_t* series,
+                    uint64_t series_stride, uint64_t series_bit0, int series_init) {
   const uint32_t words = v->n_kept / 64 + 1;
   uint64_t* next = (uint64_t*)malloc(sizeof(uint64_t) * words);
   if (!next) return 3;
+  if (kappa == 0) kappa = 1;
+  if (kappa > 63) return 1; /* phase is carried in 6 bits */
   for (uint32_t t = 0; t < n_traj; ++t) {
     uint64_t* s = states_inout + (uint64_t)t * words;
     uint64_t* cnt = counts_out + (uint64_t)t * PBN_COUNT_FIELDS;
     uint64_t* nc = node_counts_out ? node_counts_out + (uint64_t)t * v->n_kept : 0;
+    uint32_t* ser = series ? series + (uint64_t)t * series_stride : 0;
     memset(cnt, 0, sizeof(uint64_t) * PBN_COUNT_FIELDS);
     if (nc) memset(nc, 0, sizeof(uint64_t) * v->n_kept);
     orc_stream rng;
     orc_stream_init(&rng, seed, (uint32_t)(traj_begin + t), stream_kind, v->pert_groups);
-    int prev = n_pred ? orc_pred(s, pred_bits, pred_vals, n_pred) : 0;
+    const int z0 = n_pred ? orc_pred(s, pred_bits, pred_vals, n_pred) : 0;
+    int prev = 2;
+    uint32_t phase = 0; /* steps since the last sample */
+    if (thin_mode == 0) prev = z0;
+    if (thin_mode == 1 && tprev) {
+      prev = tprev[t] & 3;
+      phase = tprev[t] >> 2;
+    }
+    if (ser && series_init && series_bit0 > 0 && z0)
+      ser[(series_bit0 - 1) >> 5] |= 1u << ((series_bit0 - 1) & 31);
     for (uint64_t k = 0; k < n_steps; ++k) {
       orc_stream_begin_step(&rng, step_begin + k);
       const int cls = orc_grouped_step(v, s, next, words, &rng);
@@ -128,14 +153,28 @@ int orc_simulate(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, uin
       if (n_pred) {
         const int cur = orc_pred(s, pred_bits, pred_vals, n_pred);
         cnt[PBN_C_HITS] += (uint64_t)cur;
-        cnt[PBN_C_T00 + 2 * prev + cur]++;
-        prev = cur;
+        if (ser && cur) ser[(series_bit0 + k) >> 5] |= 1u << ((series_bit0 + k) & 31);
+        if (++phase == kappa) {
+          phase = 0;
+          if (prev != 2) cnt[PBN_C_T00 + 2 * prev + cur]++;
+          prev = cur;
+        }
       }
     }
+    if (tprev) tprev[t] = (uint8_t)(prev | (phase << 2));
     cnt[PBN_C_STEPS] = n_steps;
   }
   free(next);
   return 0;
+}
+
+int orc_simulate(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, uint32_t n_traj,
+                 int stream_kind, uint64_t step_begin, uint64_t n_steps,
+                 const uint32_t* pred_bits, const uint8_t* pred_vals, uint32_t n_pred,
+                 uint64_t* states_inout, uint64_t* counts_out, uint64_t* node_counts_out) {
+  return orc_simulate_ex(v, seed, traj_begin, n_traj, stream_kind, step_begin, n_steps, pred_bits,
+                         pred_vals, n_pred, states_inout, counts_out, node_counts_out, 1, 0, 0, 0,
+                         0, 0, 0);
 }
 
 /* Single forced step with an explicit list of uniforms (the scripted_rng

@@ -95,7 +95,40 @@ class RunArgs(C.Structure):
         ("stream", C.c_uint32), ("step_begin", C.c_uint64), ("n_steps", C.c_uint64),
         ("pred_bits", C.POINTER(C.c_uint32)), ("pred_vals", C.POINTER(C.c_uint8)),
         ("n_pred", C.c_uint32), ("flags", C.c_uint32),
+        ("kappa", C.c_uint32), ("thin_mode", C.c_uint32), ("tprev", C.POINTER(C.c_uint8)),
+        ("series", C.POINTER(C.c_uint32)), ("series_stride", C.c_uint64),
+        ("series_bit0", C.c_uint64), ("series_init", C.c_uint32), ("reserved", C.c_uint32),
     ]
+
+
+class EstimateRequest(C.Structure):
+    _fields_ = [
+        ("precision", C.c_double), ("confidence", C.c_double), ("pilot", C.c_uint64),
+        ("burn_epsilon", C.c_double), ("max_refinements", C.c_uint32),
+        ("sample_inflation", C.c_double), ("seed", C.c_uint64), ("traj_begin", C.c_uint64),
+        ("n_traj", C.c_uint32), ("stream", C.c_uint32),
+    ]
+
+
+class EstimateResult(C.Structure):
+    _fields_ = [
+        ("estimate", C.c_double), ("sample_size_used", C.c_uint64), ("burn_in_used", C.c_uint64),
+        ("steps_per_traj", C.c_uint64), ("kappa", C.c_uint32), ("degenerate", C.c_uint32),
+        ("alpha", C.c_double), ("beta", C.c_double), ("wall_seconds", C.c_double),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+RUN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                     C.c_uint64, C.c_uint32, C.POINTER(C.c_uint64))
+STATS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64))
+
+
+class EstimatorBackend(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("n_traj", C.c_uint32), ("reserved", C.c_uint32),
+                ("series_capacity", C.c_uint64), ("run", RUN_FN), ("series_stats", STATS_FN)]
 
 
 def _load():
@@ -136,7 +169,12 @@ def _load():
         "pbn_gpu_last_launches": (U32, [P]),
         "pbn_gpu_destroy": (None, [P]),
         "pbn_philox_kat": (I, [C.POINTER(U32), U32, U64, C.POINTER(U32)]),
-        "pbn_estimate": (I, [P, P, P, P, U32, P, P]),
+        "pbn_estimate": (I, [P, C.POINTER(EstimateRequest), C.POINTER(U32), C.POINTER(C.c_uint8),
+                             U32, C.POINTER(U64), C.POINTER(EstimateResult)]),
+        "pbn_estimate_with_backend": (I, [C.POINTER(EstimateRequest), C.POINTER(EstimatorBackend),
+                                          C.POINTER(EstimateResult)]),
+        "pbn_series_stats_host": (I, [C.POINTER(U32), U32, U64, U64, U32, C.POINTER(U64)]),
+        "pbn_inverse_normal_cdf": (C.c_double, [C.c_double]),
         "pbn_internal_lower_bound": (U32, [C.POINTER(U32), U32, U64]),
         "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
         "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
@@ -156,6 +194,7 @@ EXPORTED_SYMBOLS = (
     "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
     "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
     "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_destroy", "pbn_estimate",
+    "pbn_estimate_with_backend", "pbn_series_stats_host", "pbn_inverse_normal_cdf",
 )
 
 
@@ -439,9 +478,12 @@ class GpuEnsemble:
         return a
 
     def simulate(self, seed, n_traj, n_steps, traj_begin=0, step_begin=0, states=None,
-                 pred=None, stream=STREAM_U53):
+                 pred=None, stream=STREAM_U53, kappa=1, thin_mode=0, tprev=None, series=None,
+                 series_bit0=0, series_init=False):
         """HOST buffers in/out. states: (n_traj, words) uint64 engine-order (zeros if None).
         pred: (engine bits, values) from PreparedSimulation.compile_predicate.
+        kappa/thin_mode/tprev: sampled predicate transitions (see pbn_run_args);
+        series: (n_traj, stride) uint32 bit rows updated in place.
         Returns (states, counts[n_traj, 8])."""
         if states is None:
             states = np.zeros((n_traj, self.words), np.uint64)
@@ -449,6 +491,15 @@ class GpuEnsemble:
         assert states.shape == (n_traj, self.words)
         counts = np.zeros((n_traj, COUNT_FIELDS), np.uint64)
         a = self._args(seed, traj_begin, n_traj, n_steps, step_begin, pred, stream)
+        a.kappa, a.thin_mode = kappa, thin_mode
+        if tprev is not None:
+            assert tprev.dtype == np.uint8 and tprev.flags.c_contiguous and len(tprev) == n_traj
+            a.tprev = tprev.ctypes.data_as(C.POINTER(C.c_uint8))
+        if series is not None:
+            assert series.dtype == np.uint32 and series.flags.c_contiguous
+            a.series = _u32p(series)
+            a.series_stride = series.shape[1]
+            a.series_bit0, a.series_init = series_bit0, 1 if series_init else 0
         _check(lib.pbn_gpu_run(self._h, C.byref(a), _u64p(states), _u64p(counts), None))
         return states, counts
 
@@ -461,3 +512,70 @@ class GpuEnsemble:
 
     def last_launches(self) -> int:
         return int(lib.pbn_gpu_last_launches(self._h))
+
+
+# ----------------------------------------------------------------------------
+# Pooled two-state Markov chain steady-state estimate (estimator.hpp:137-244)
+
+def make_request(precision=1e-3, confidence=0.95, pilot=10000, burn_epsilon=0.0,
+                 max_refinements=20, sample_inflation=1.3, seed=42, traj_begin=0, n_traj=1,
+                 stream=STREAM_U53):
+    """estimation_request (estimator.hpp:59-70) + ensemble fields."""
+    return EstimateRequest(precision, confidence, pilot, burn_epsilon, max_refinements,
+                           sample_inflation, seed, traj_begin, n_traj, stream)
+
+
+def estimate(engine: "GpuEnsemble", pred, req: EstimateRequest, states=None):
+    """Device ensemble estimate of P(predicate) under the stationary law.
+    pred: (engine bits, values); states: (n_traj, words) initial states (zeros)."""
+    n = req.n_traj
+    st = (np.zeros((n, engine.words), np.uint64) if states is None
+          else np.ascontiguousarray(states, np.uint64).copy())
+    bits = np.ascontiguousarray(pred[0], np.uint32)
+    vals = np.ascontiguousarray(pred[1], np.uint8)
+    res = EstimateResult()
+    _check(lib.pbn_estimate(engine._h, C.byref(req), _u32p(bits),
+                            vals.ctypes.data_as(C.POINTER(C.c_uint8)), len(bits), _u64p(st),
+                            C.byref(res)))
+    return res.as_dict(), st
+
+
+def estimate_with_backend(req: EstimateRequest, n_traj, run, series_stats, series_capacity):
+    """The same C++ estimator over Python callbacks (tests: the oracle as stepper).
+    run(step_begin, n_steps, kappa, thin_mode, series_bit0|None, series_init) -> totals[8];
+    series_stats(kappa, length) -> 13 pooled counters."""
+
+    def _run(user, s0, n, kappa, mode, bit0, init, out):
+        try:
+            tot = run(s0, n, kappa, mode, None if bit0 == (1 << 64) - 1 else bit0, bool(init))
+            for i in range(8):
+                out[i] = int(tot[i])
+            return 0
+        except Exception:  # noqa: BLE001  (reported as a backend failure)
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def _stats(user, kappa, length, out):
+        try:
+            v = series_stats(kappa, length)
+            for i in range(13):
+                out[i] = int(v[i])
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    be = EstimatorBackend(None, n_traj, 0, series_capacity, RUN_FN(_run), STATS_FN(_stats))
+    res = EstimateResult()
+    _check(lib.pbn_estimate_with_backend(C.byref(req), C.byref(be), C.byref(res)))
+    return res.as_dict()
+
+
+def series_stats_host(series: np.ndarray, length: int, kappa: int):
+    out = np.zeros(13, np.uint64)
+    ser = np.ascontiguousarray(series, np.uint32)
+    _check(lib.pbn_series_stats_host(_u32p(ser), ser.shape[0], ser.shape[1], length, kappa,
+                                     _u64p(out)))
+    return out

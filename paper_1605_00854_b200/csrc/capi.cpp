@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -14,6 +15,7 @@
 #include "../../include/pbn_b200.h"
 #include "device/dev_plan.h"
 #include "host/device_plan.hpp"
+#include "host/estimator.hpp"
 #include "host/generator.hpp"
 #include "host/model.hpp"
 #include "host/plan.hpp"
@@ -26,6 +28,11 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             std::uint32_t* launches);
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
                               std::uint32_t n, cudaStream_t stream);
+cudaError_t launch_series_stats(const std::uint32_t* d_series, std::uint32_t n_traj,
+                                std::uint64_t stride, std::uint64_t len, std::uint32_t kappa,
+                                unsigned long long* d_out13, cudaStream_t stream);
+cudaError_t launch_sum_counts(const std::uint64_t* d_counts, std::uint32_t n,
+                              unsigned long long* d_out8, cudaStream_t stream);
 }  // namespace pbn_b200
 
 using namespace pbn_b200;
@@ -141,6 +148,19 @@ dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
     throw resource_error("U32 stream needs every group alias table <= 2^21 cells");
   if (a.flags & PBN_RUN_NODE_COUNTS)
     throw std::invalid_argument("per-node counts are not implemented on the device yet");
+  if (a.n_steps > 0xFFFFFFFFull)
+    throw std::invalid_argument("at most 2^32-1 steps per call (chain calls with step_begin)");
+  if (a.thin_mode > 2) throw std::invalid_argument("thin_mode must be 0, 1 or 2");
+  rp.kappa = a.kappa ? a.kappa : 1;
+  if (rp.kappa > 63) throw std::invalid_argument("kappa must be <= 63");
+  rp.thin_mode = a.thin_mode;
+  rp.tprev = a.tprev;
+  rp.series = a.series;
+  rp.series_stride = a.series_stride;
+  rp.series_bit0 = a.series_bit0;
+  rp.series_init = a.series_init;
+  if (a.series && (a.series_bit0 + a.n_steps + 31) / 32 > a.series_stride)
+    throw std::invalid_argument("series row too short for this call");
   if (a.traj_begin + a.n_traj > (1ull << 32))
     throw std::invalid_argument("trajectory ids must fit in 32 bits");
   return rp;
@@ -418,8 +438,31 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* c
     }
     if (a->n_traj == 0) return;
     ck(cudaMemcpy(g->d_states, states, 8 * words * a->n_traj, cudaMemcpyHostToDevice), "H2D");
-    run_device(*g, *a, g->d_states, g->d_counts, nullptr);
+    // optional per-trajectory buffers: host -> device copies around the launch
+    pbn_run_args da = *a;
+    std::uint8_t* d_tprev = nullptr;
+    std::uint32_t* d_series = nullptr;
+    const std::size_t series_bytes = 4 * a->series_stride * a->n_traj;
+    struct scratch {
+      void* p = nullptr;
+      ~scratch() { if (p) cudaFree(p); }
+    } s1, s2;
+    if (a->tprev) {
+      ck(cudaMalloc(&d_tprev, a->n_traj), "cudaMalloc tprev");
+      s1.p = d_tprev;
+      ck(cudaMemcpy(d_tprev, a->tprev, a->n_traj, cudaMemcpyHostToDevice), "H2D");
+      da.tprev = d_tprev;
+    }
+    if (a->series) {
+      ck(cudaMalloc(&d_series, series_bytes), "cudaMalloc series");
+      s2.p = d_series;
+      ck(cudaMemcpy(d_series, a->series, series_bytes, cudaMemcpyHostToDevice), "H2D");
+      da.series = d_series;
+    }
+    run_device(*g, da, g->d_states, g->d_counts, nullptr);
     ck(cudaMemcpy(states, g->d_states, 8 * words * a->n_traj, cudaMemcpyDeviceToHost), "D2H");
+    if (a->tprev) ck(cudaMemcpy(a->tprev, d_tprev, a->n_traj, cudaMemcpyDeviceToHost), "D2H");
+    if (a->series) ck(cudaMemcpy(a->series, d_series, series_bytes, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(counts, g->d_counts, 8 * PBN_COUNT_FIELDS * static_cast<std::size_t>(a->n_traj),
                   cudaMemcpyDeviceToHost),
        "D2H");
@@ -484,6 +527,128 @@ int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint3
   });
 }
 
+}  // extern "C"
+
+// ---- estimator backends --------------------------------------------------------
+namespace {
+
+template <class T>
+struct dev_buf {
+  T* p = nullptr;
+  explicit dev_buf(std::size_t n) { ck(cudaMalloc(&p, sizeof(T) * (n ? n : 1)), "cudaMalloc"); }
+  ~dev_buf() {
+    if (p) cudaFree(p);
+  }
+  dev_buf(const dev_buf&) = delete;
+  dev_buf& operator=(const dev_buf&) = delete;
+};
+
+// Device ensemble: states, carried thin samples, pilot series and count
+// records stay in HBM; each round returns 8 pooled counters.
+class device_backend : public estimator_backend {
+ public:
+  device_backend(pbn_gpu& g, const pbn_estimate_request& req, const std::uint32_t* bits,
+                 const std::uint8_t* vals, std::uint32_t n_pred)
+      : g_(g), req_(req), bits_(bits), vals_(vals), n_pred_(n_pred),
+        words_(pbn_state_words(g.ep.h.n_kept)),
+        cap_(std::min<std::uint64_t>(1ull << 22,
+                                     std::max<std::uint64_t>(1024, (1ull << 33) / std::max(1u, req.n_traj)))),
+        stride_((cap_ + 31) / 32),
+        states_(static_cast<std::size_t>(req.n_traj) * words_),
+        counts_(static_cast<std::size_t>(req.n_traj) * PBN_COUNT_FIELDS),
+        tprev_(req.n_traj),
+        series_(static_cast<std::size_t>(req.n_traj) * stride_),
+        red_(16) {
+    ck(cudaMemset(series_.p, 0, sizeof(std::uint32_t) * req.n_traj * stride_), "memset");
+  }
+  std::uint32_t n_traj() const override { return req_.n_traj; }
+  std::uint64_t series_capacity() const override { return cap_; }
+  void upload(const std::uint64_t* host) {
+    ck(cudaMemcpy(states_.p, host, 8 * words_ * req_.n_traj, cudaMemcpyHostToDevice), "H2D");
+  }
+  void download(std::uint64_t* host) {
+    ck(cudaMemcpy(host, states_.p, 8 * words_ * req_.n_traj, cudaMemcpyDeviceToHost), "D2H");
+  }
+  void run(std::uint64_t step_begin, std::uint64_t n_steps, std::uint32_t kappa,
+           std::uint32_t thin_mode, std::uint64_t series_bit0, bool series_init,
+           std::uint64_t totals[PBN_COUNT_FIELDS]) override {
+    for (int i = 0; i < PBN_COUNT_FIELDS; ++i) totals[i] = 0;
+    std::uint64_t done = 0;
+    while (done < n_steps) {  // at most 2^31 steps per launch
+      const std::uint64_t n = std::min<std::uint64_t>(n_steps - done, 1ull << 31);
+      pbn_run_args a{};
+      a.seed = req_.seed;
+      a.traj_begin = req_.traj_begin;
+      a.n_traj = req_.n_traj;
+      a.stream = req_.stream;
+      a.step_begin = step_begin + done;
+      a.n_steps = n;
+      a.pred_bits = bits_;
+      a.pred_vals = vals_;
+      a.n_pred = n_pred_;
+      a.kappa = kappa;
+      a.thin_mode = done == 0 ? thin_mode : 1u;
+      a.tprev = tprev_.p;
+      if (series_bit0 != std::numeric_limits<std::uint64_t>::max()) {
+        a.series = series_.p;
+        a.series_stride = stride_;
+        a.series_bit0 = series_bit0 + done;
+        a.series_init = done == 0 && series_init;
+      }
+      run_device(g_, a, states_.p, counts_.p, nullptr);
+      ck(launch_sum_counts(counts_.p, req_.n_traj, red_.p, nullptr), "sum counts");
+      unsigned long long t[8];
+      ck(cudaMemcpy(t, red_.p, sizeof t, cudaMemcpyDeviceToHost), "D2H");
+      for (int i = 0; i < 8; ++i) totals[i] += t[i];
+      done += n;
+    }
+  }
+  void series_stats(std::uint32_t kappa, std::uint64_t len, std::uint64_t out[13]) override {
+    ck(launch_series_stats(series_.p, req_.n_traj, stride_, len, kappa, red_.p, nullptr),
+       "series stats");
+    unsigned long long t[13];
+    ck(cudaMemcpy(t, red_.p, sizeof t, cudaMemcpyDeviceToHost), "D2H");
+    for (int i = 0; i < 13; ++i) out[i] = t[i];
+  }
+
+ private:
+  pbn_gpu& g_;
+  pbn_estimate_request req_;
+  const std::uint32_t* bits_;
+  const std::uint8_t* vals_;
+  std::uint32_t n_pred_;
+  std::uint64_t words_, cap_, stride_;
+  dev_buf<std::uint64_t> states_, counts_;
+  dev_buf<std::uint8_t> tprev_;
+  dev_buf<std::uint32_t> series_;
+  dev_buf<unsigned long long> red_;
+};
+
+class callback_backend : public estimator_backend {
+ public:
+  explicit callback_backend(const pbn_estimator_backend& b) : b_(b) {}
+  std::uint32_t n_traj() const override { return b_.n_traj; }
+  std::uint64_t series_capacity() const override { return b_.series_capacity; }
+  void run(std::uint64_t step_begin, std::uint64_t n_steps, std::uint32_t kappa,
+           std::uint32_t thin_mode, std::uint64_t series_bit0, bool series_init,
+           std::uint64_t totals[PBN_COUNT_FIELDS]) override {
+    if (b_.run(b_.user, step_begin, n_steps, kappa, thin_mode, series_bit0, series_init ? 1 : 0,
+               totals) != 0)
+      throw std::runtime_error("estimator backend run failed");
+  }
+  void series_stats(std::uint32_t kappa, std::uint64_t len, std::uint64_t out[13]) override {
+    if (b_.series_stats(b_.user, kappa, len, out) != 0)
+      throw std::runtime_error("estimator backend series_stats failed");
+  }
+
+ private:
+  pbn_estimator_backend b_;
+};
+
+}  // namespace
+
+extern "C" {
+
 int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pred_bits,
                  const uint8_t* pred_vals, uint32_t n_pred, uint64_t* states_inout,
                  pbn_estimate_result* out) {
@@ -491,12 +656,43 @@ int pbn_estimate(pbn_gpu* g, const pbn_estimate_request* req, const uint32_t* pr
     need(g, "gpu");
     need(req, "request");
     need(out, "result");
-    (void)pred_bits;
-    (void)pred_vals;
-    (void)n_pred;
-    (void)states_inout;
-    throw std::invalid_argument("pbn_estimate: not implemented yet");
+    need(states_inout, "states");
+    if (n_pred == 0) throw model_error("empty predicate");
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    device_backend be(*g, *req, pred_bits, pred_vals, n_pred);
+    be.upload(states_inout);
+    *out = estimate_pooled(*req, be);
+    be.download(states_inout);
   });
+}
+
+int pbn_estimate_with_backend(const pbn_estimate_request* req, const pbn_estimator_backend* be,
+                              pbn_estimate_result* out) {
+  return guard([&] {
+    need(req, "request");
+    need(be, "backend");
+    need(out, "result");
+    callback_backend cb(*be);
+    *out = estimate_pooled(*req, cb);
+  });
+}
+
+int pbn_series_stats_host(const uint32_t* series, uint32_t n_traj, uint64_t stride, uint64_t len,
+                          uint32_t kappa, uint64_t* out13) {
+  return guard([&] {
+    need(series, "series");
+    need(out13, "out");
+    series_stats_host(series, n_traj, stride, len, kappa, out13);
+  });
+}
+
+double pbn_inverse_normal_cdf(double p) {
+  try {
+    return inverse_normal_cdf(p);
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return std::numeric_limits<double>::quiet_NaN();
+  }
 }
 
 }  // extern "C"

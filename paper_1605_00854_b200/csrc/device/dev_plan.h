@@ -78,6 +78,20 @@ struct dev_run_params {
   std::uint64_t step_begin;
   std::uint64_t n_steps;
   dev_predicate pred;
+  // predicate-process statistics (estimator.hpp:76-102): transitions between
+  // samples taken every `kappa`-th step; first previous sample = the input
+  // state's predicate with phase 0 (thin_mode 0), carried over from
+  // tprev[traj] = prev | phase << 2 (1; prev 2 = none), or none (2)
+  std::uint32_t kappa;
+  std::uint32_t thin_mode;
+  std::uint8_t* tprev;          // per trajectory, in/out, may be null
+  // optional series of predicate bits: step i -> bit series_bit0 + i of the
+  // trajectory's row; series_init: the input state's bit at series_bit0 - 1
+  std::uint32_t* series;
+  std::uint64_t series_stride;  // u32 words per trajectory row
+  std::uint64_t series_bit0;
+  std::uint32_t series_init;
+  std::uint32_t pad1;
 };
 
 }  // namespace pbn_b200

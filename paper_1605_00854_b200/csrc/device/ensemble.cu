@@ -347,8 +347,21 @@ __global__ void __launch_bounds__(1024, 1)
   };
 
   std::uint32_t cur = 0;
-  std::uint32_t prev = pred_eval(S0);
-  std::uint32_t n01 = 0, n10 = 0, n11 = 0, nfn = 0, npert = 0;
+  const std::uint32_t z0 = pred_eval(S0);
+  std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
+  if (rp.thin_mode == 0) prev = z0;
+  if (rp.thin_mode == 1 && rp.tprev) {
+    const std::uint32_t tp = rp.tprev[tloc];
+    prev = tp & 3u;
+    kphase = tp >> 2;
+  }
+  std::uint32_t n00 = 0, n01 = 0, n10 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
+  std::uint32_t* ser = rp.series ? rp.series + tloc * rp.series_stride : nullptr;
+  std::uint32_t sword = 0;   // series bits of the current word (lane r == 0)
+  if (ser && r == 0 && rp.series_init && rp.series_bit0 > 0 && z0) {
+    const std::uint64_t p0 = rp.series_bit0 - 1;
+    ser[p0 >> 5] |= 1u << (p0 & 31);
+  }
   const std::uint64_t s_end = rp.step_begin + rp.n_steps;
 
   for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
@@ -446,14 +459,28 @@ __global__ void __launch_bounds__(1024, 1)
       ++nfn;
     }
 
-    // ---- statistics (engine.hpp:375-381) + predicate transitions
+    // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
     const std::uint32_t hit = pred_eval(cur ? S1 : S0);
-    n01 += (prev == 0) & (hit == 1);
-    n10 += (prev == 1) & (hit == 0);
-    n11 += (prev == 1) & (hit == 1);
-    prev = hit;
+    nhit += hit;
+    if (++kphase == rp.kappa) {
+      kphase = 0;
+      n00 += (prev == 0) & (hit == 0);
+      n01 += (prev == 0) & (hit == 1);
+      n10 += (prev == 1) & (hit == 0);
+      n11 += (prev == 1) & (hit == 1);
+      prev = hit;
+    }
+    if (ser != nullptr && r == 0) {  // launch-uniform branch
+      const std::uint64_t pos = rp.series_bit0 + (s - rp.step_begin);
+      sword |= hit << (pos & 31);
+      if ((pos & 31) == 31 || s + 1 == s_end) {
+        if (sword) ser[pos >> 5] |= sword;
+        sword = 0;
+      }
+    }
     __syncwarp(smask);
   }
+  if (rp.tprev && r == 0) rp.tprev[tloc] = static_cast<std::uint8_t>(prev | (kphase << 2));
 
   {
     const std::uint32_t* Sf = cur ? S1 : S0;
@@ -462,17 +489,86 @@ __global__ void __launch_bounds__(1024, 1)
   }
   if (r == 0) {
     std::uint64_t* c = counts + tloc * 8;
-    const std::uint64_t steps = rp.n_steps;
-    const std::uint64_t t11 = n11, t01 = n01, t10 = n10;
-    c[0] = steps;
-    c[1] = rp.pred.n ? t01 + t11 : 0;
-    c[2] = rp.pred.n ? steps - t01 - t10 - t11 : 0;
-    c[3] = rp.pred.n ? t01 : 0;
-    c[4] = rp.pred.n ? t10 : 0;
-    c[5] = rp.pred.n ? t11 : 0;
+    const bool pr = rp.pred.n != 0;
+    c[0] = rp.n_steps;
+    c[1] = pr ? nhit : 0;
+    c[2] = pr ? n00 : 0;
+    c[3] = pr ? n01 : 0;
+    c[4] = pr ? n10 : 0;
+    c[5] = pr ? n11 : 0;
     c[6] = nfn;
     c[7] = npert;
   }
+}
+
+// Pooled statistics of stored predicate series (estimator pilot): per
+// trajectory row, triple counts n_ijk at period kappa (t = 2k, 3k, ...), thinned
+// pair counts (t = k, 2k, ...) and ones in [1, len); summed over trajectories.
+__global__ void pbn_series_stats_kernel(const std::uint32_t* __restrict__ series,
+                                        std::uint32_t n_traj, std::uint64_t stride,
+                                        std::uint64_t len, std::uint32_t kappa,
+                                        unsigned long long* __restrict__ out) {
+  const std::uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c[13];
+#pragma unroll
+  for (int i = 0; i < 13; ++i) c[i] = 0;
+  if (t < n_traj) {
+    const std::uint32_t* row = series + t * stride;
+    auto z = [&](std::uint64_t i) -> std::uint32_t { return (__ldg(row + (i >> 5)) >> (i & 31)) & 1u; };
+    for (std::uint64_t i = 2ull * kappa; i < len; i += kappa) {
+      const std::uint32_t idx = (z(i - 2 * kappa) << 2) | (z(i - kappa) << 1) | z(i);
+#pragma unroll
+      for (std::uint32_t q = 0; q < 8; ++q) c[q] += idx == q;
+    }
+    for (std::uint64_t i = kappa; i < len; i += kappa) {
+      const std::uint32_t idx = (z(i - kappa) << 1) | z(i);
+#pragma unroll
+      for (std::uint32_t q = 0; q < 4; ++q) c[8 + q] += idx == q;
+    }
+    for (std::uint64_t w = 0; w * 32 < len; ++w) {
+      std::uint32_t word = __ldg(row + w);
+      if (w == 0) word &= ~1u;  // position 0 is the initial state
+      const std::uint64_t end = len - w * 32;
+      if (end < 32) word &= (1u << end) - 1u;
+      c[12] += __popc(word);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 13; ++i) {
+    unsigned long long v = c[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + i, v);
+  }
+}
+
+// Sum of per-trajectory count records (n x 8) into out[8].
+__global__ void pbn_sum_counts_kernel(const std::uint64_t* __restrict__ counts, std::uint32_t n,
+                                      unsigned long long* __restrict__ out) {
+  const std::uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int f = 0; f < 8; ++f) {
+    unsigned long long v = t < n ? counts[static_cast<std::uint64_t>(t) * 8 + f] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + f, v);
+  }
+}
+
+cudaError_t launch_series_stats(const std::uint32_t* d_series, std::uint32_t n_traj,
+                                std::uint64_t stride, std::uint64_t len, std::uint32_t kappa,
+                                unsigned long long* d_out13, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(d_out13, 0, 13 * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  pbn_series_stats_kernel<<<(n_traj + 255) / 256, 256, 0, stream>>>(d_series, n_traj, stride, len,
+                                                                    kappa, d_out13);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_counts(const std::uint64_t* d_counts, std::uint32_t n,
+                              unsigned long long* d_out8, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(d_out8, 0, 8 * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  pbn_sum_counts_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_counts, n, d_out8);
+  return cudaGetLastError();
 }
 
 // Known-answer kernel for the stream: out[i] = Philox4x32-10(ctr[i], key).

@@ -61,5 +61,23 @@ def main():
         json.dump(manifest, f, indent=1, sort_keys=True)
 
 
+
+
+def steady_state_reference():
+    """High-precision steady-state value of the c3 target under the reference's
+    own single-chain estimator (xoshiro256, r = 2.5e-4): the yardstick the
+    pooled device estimate at r = 1e-3 is compared against."""
+    ref = oracle.Reference()
+    text, terms = config_text("c3")
+    rplan = ref.parse(text).prepare(1 << 25, 12, 8)
+    est = rplan.estimate(terms, 2.5e-4, 0.95, 10000, 2024, -1, 0)
+    out = {"config": "c3", "k_max": 12, "mgp": 8, "precision": 2.5e-4, "confidence": 0.95,
+           "seed": 2024, "terms": terms, **est}
+    with open(os.path.join(HERE, "c3_steady_state.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("c3 steady state", est, flush=True)
+
+
 if __name__ == "__main__":
     main()
+    steady_state_reference()
