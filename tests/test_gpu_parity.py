@@ -119,3 +119,30 @@ def test_philox_device_matches_oracle(pb, orc, cuda_ok):
     key = np.array([seed & 0xFFFFFFFF, seed >> 32], np.uint32)
     for i in range(len(ctr)):
         assert np.array_equal(dev[i], orc.philox(ctr[i], key))
+
+
+@pytest.mark.parametrize("kappa,mode", [(1, 0), (3, 0), (4, 1), (7, 2), (16, 1)])
+def test_sampled_transitions_and_series_vs_oracle(pb, orc, cuda_ok, kappa, mode):
+    """Estimator statistics: kappa-thinned transitions with the sample and its
+    phase carried in tprev across calls, and the recorded predicate series."""
+    plan, pred = _setup(pb, "c3")
+    eng = pb.GpuEnsemble(plan)
+    n, steps = 70, 333
+    tp_d = np.full(n, 2 | (1 << 2), np.uint8)
+    tp_o = tp_d.copy()
+    ser_d = np.zeros((n, 40), np.uint32)
+    ser_o = ser_d.copy()
+    st_d = st_o = None
+    for call in range(3):
+        st_d, c_d = eng.simulate(seed=4, n_traj=n, n_steps=steps, step_begin=call * steps,
+                                 states=st_d, pred=pred, kappa=kappa, thin_mode=mode if call == 0 else 1,
+                                 tprev=tp_d, series=ser_d, series_bit0=1 + call * steps,
+                                 series_init=call == 0)
+        st_o, c_o = orc.simulate_ex(plan.view, 4, 0, n, steps, states=st_o, step_begin=call * steps,
+                                    pred=pred, kappa=kappa, thin_mode=mode if call == 0 else 1,
+                                    tprev=tp_o, series=ser_o, series_bit0=1 + call * steps,
+                                    series_init=call == 0)
+        assert np.array_equal(c_d, c_o)
+        assert np.array_equal(st_d, st_o)
+        assert np.array_equal(tp_d, tp_o)
+    assert np.array_equal(ser_d, ser_o)
