@@ -200,7 +200,8 @@ int pbn_gpu_info(const pbn_gpu* g, uint32_t* lanes_per_traj, uint32_t* tables_in
                  uint64_t* smem_bytes, uint64_t* plan_bytes, uint32_t* warps_per_cta);
 /* End-to-end: HOST buffers. states_inout: n_traj * pbn_state_words(n_kept) uint64,
  * counts_out: n_traj * PBN_COUNT_FIELDS uint64, node_counts_out (flag NODE_COUNTS):
- * n_traj * n_kept uint64 or NULL. Synchronous. */
+ * n_traj * n_kept uint64 one-counts of the call (engine.hpp:378-379), or NULL.
+ * Synchronous. (pbn_gpu_run_device ADDS into d_node_counts.) */
 int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states_inout, uint64_t* counts_out,
                 uint64_t* node_counts_out);
 /* Device-resident: DEVICE pointers, asynchronous on `stream` (a cudaStream_t, 0 = legacy). */

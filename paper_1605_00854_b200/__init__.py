@@ -32,6 +32,7 @@ LIB_PATH = os.path.join(_HERE, "libpbn_b200.so")
 
 STREAM_U53 = 0
 STREAM_U32 = 1
+RUN_NODE_COUNTS = 1
 COUNT_FIELDS = 8
 C_STEPS, C_HITS, C_T00, C_T01, C_T10, C_T11, C_FNSTEPS, C_PERTSTEPS = range(8)
 DEFAULT_THETA = 1 << 25  # engine.hpp:81
@@ -479,7 +480,7 @@ class GpuEnsemble:
 
     def simulate(self, seed, n_traj, n_steps, traj_begin=0, step_begin=0, states=None,
                  pred=None, stream=STREAM_U53, kappa=1, thin_mode=0, tprev=None, series=None,
-                 series_bit0=0, series_init=False):
+                 series_bit0=0, series_init=False, node_counts=False):
         """HOST buffers in/out. states: (n_traj, words) uint64 engine-order (zeros if None).
         pred: (engine bits, values) from PreparedSimulation.compile_predicate.
         kappa/thin_mode/tprev: sampled predicate transitions (see pbn_run_args);
@@ -500,8 +501,13 @@ class GpuEnsemble:
             a.series = _u32p(series)
             a.series_stride = series.shape[1]
             a.series_bit0, a.series_init = series_bit0, 1 if series_init else 0
-        _check(lib.pbn_gpu_run(self._h, C.byref(a), _u64p(states), _u64p(counts), None))
-        return states, counts
+        nc = None
+        if node_counts:
+            a.flags |= RUN_NODE_COUNTS
+            nc = np.zeros((n_traj, self.n_kept), np.uint64)
+        _check(lib.pbn_gpu_run(self._h, C.byref(a), _u64p(states), _u64p(counts),
+                               _u64p(nc) if nc is not None else None))
+        return (states, counts, nc) if node_counts else (states, counts)
 
     def simulate_device(self, seed, n_traj, n_steps, d_states, d_counts, traj_begin=0,
                         step_begin=0, pred=None, stream=STREAM_U53, cuda_stream=0):

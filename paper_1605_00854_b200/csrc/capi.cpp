@@ -118,11 +118,13 @@ std::uint32_t staged_bytes(const pbn_gpu& g) {
 
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
-std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt) {
+std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt,
+                         bool node_counts) {
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(32, w));
-  const std::uint64_t stride = (2 * g.ep.h.sw32 + lpt * 4 + 3) & ~3u;
+  const std::uint64_t stride =
+      (2 * g.ep.h.sw32 + lpt * 4 + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
   const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
   while (w > 1 && w * per_warp > avail) --w;
@@ -146,8 +148,6 @@ dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
     throw std::invalid_argument("unknown stream kind");
   if (a.stream == PBN_STREAM_U32 && !g.ep.h.u32_ok)
     throw resource_error("U32 stream needs every group alias table <= 2^21 cells");
-  if (a.flags & PBN_RUN_NODE_COUNTS)
-    throw std::invalid_argument("per-node counts are not implemented on the device yet");
   if (a.n_steps > 0xFFFFFFFFull)
     throw std::invalid_argument("at most 2^32-1 steps per call (chain calls with step_begin)");
   if (a.thin_mode > 2) throw std::invalid_argument("thin_mode must be 0, 1 or 2");
@@ -167,16 +167,35 @@ dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
 }
 
 void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
-                std::uint64_t* d_counts, cudaStream_t stream) {
-  const dev_run_params rp = make_params(g, a);
+                std::uint64_t* d_counts, std::uint64_t* d_node_counts, cudaStream_t stream) {
+  dev_run_params rp = make_params(g, a);
   if (a.n_traj == 0) return;
+  const bool nc = (a.flags & PBN_RUN_NODE_COUNTS) != 0;
+  if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
+  rp.node_counts = nc ? d_node_counts : nullptr;
   ck(cudaSetDevice(g.device), "cudaSetDevice");
   g.last_lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
-  g.last_warps = pick_warps(g, a.n_traj, g.last_lpt);
+  // the counter planes take shared memory: fall back to a leaner plan
+  // placement if the ensemble no longer fits next to the staged plan
+  const int place0 = g.place;
+  for (;;) {
+    try {
+      g.last_warps = pick_warps(g, a.n_traj, g.last_lpt, nc);
+      break;
+    } catch (const resource_error&) {
+      if (g.place == 0) {
+        g.place = place0;
+        throw;
+      }
+      --g.place;
+    }
+  }
   g.launches = 0;
-  ck(launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_lpt,
-                     g.last_warps, rp, d_states, d_counts, stream, &g.launches),
-     "ensemble launch");
+  const cudaError_t e = launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream),
+                                        g.last_lpt, g.last_warps, rp, d_states, d_counts, stream,
+                                        &g.launches);
+  g.place = place0;
+  ck(e, "ensemble launch");
 }
 
 }  // namespace
@@ -423,7 +442,6 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* c
     need(a, "args");
     need(states, "states");
     need(counts, "counts");
-    (void)node_counts;
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     const std::size_t words = pbn_state_words(g->ep.h.n_kept);
     if (a->n_traj > g->cap_traj) {
@@ -459,7 +477,20 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* c
       ck(cudaMemcpy(d_series, a->series, series_bytes, cudaMemcpyHostToDevice), "H2D");
       da.series = d_series;
     }
-    run_device(*g, da, g->d_states, g->d_counts, nullptr);
+    std::uint64_t* d_nc = nullptr;
+    struct scratch3 {
+      void* p = nullptr;
+      ~scratch3() { if (p) cudaFree(p); }
+    } s3;
+    const std::size_t nc_bytes = 8ull * g->ep.h.n_kept * a->n_traj;
+    if (a->flags & PBN_RUN_NODE_COUNTS) {
+      need(node_counts, "node_counts");
+      ck(cudaMalloc(&d_nc, nc_bytes), "cudaMalloc node counts");
+      s3.p = d_nc;
+      ck(cudaMemset(d_nc, 0, nc_bytes), "memset");
+    }
+    run_device(*g, da, g->d_states, g->d_counts, d_nc, nullptr);
+    if (d_nc) ck(cudaMemcpy(node_counts, d_nc, nc_bytes, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(states, g->d_states, 8 * words * a->n_traj, cudaMemcpyDeviceToHost), "D2H");
     if (a->tprev) ck(cudaMemcpy(a->tprev, d_tprev, a->n_traj, cudaMemcpyDeviceToHost), "D2H");
     if (a->series) ck(cudaMemcpy(a->series, d_series, series_bytes, cudaMemcpyDeviceToHost), "D2H");
@@ -474,8 +505,7 @@ int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states, ui
   return guard([&] {
     need(g, "gpu");
     need(a, "args");
-    (void)d_node_counts;
-    run_device(*g, *a, d_states, d_counts, static_cast<cudaStream_t>(stream));
+    run_device(*g, *a, d_states, d_counts, d_node_counts, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -595,7 +625,7 @@ class device_backend : public estimator_backend {
         a.series_bit0 = series_bit0 + done;
         a.series_init = done == 0 && series_init;
       }
-      run_device(g_, a, states_.p, counts_.p, nullptr);
+      run_device(g_, a, states_.p, counts_.p, nullptr, nullptr);
       ck(launch_sum_counts(counts_.p, req_.n_traj, red_.p, nullptr), "sum counts");
       unsigned long long t[8];
       ck(cudaMemcpy(t, red_.p, sizeof t, cudaMemcpyDeviceToHost), "D2H");

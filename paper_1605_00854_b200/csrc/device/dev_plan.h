@@ -92,6 +92,9 @@ struct dev_run_params {
   std::uint64_t series_bit0;
   std::uint32_t series_init;
   std::uint32_t pad1;
+  // optional per-node one-counts (engine.hpp:378-379): n_traj x n_kept u64,
+  // accumulated (+=) over the call's steps
+  std::uint64_t* node_counts;
 };
 
 }  // namespace pbn_b200

@@ -185,16 +185,47 @@ __global__ void __launch_bounds__(1024, 1)
   // per-trajectory shared memory: two state buffers + the phase-B draw buffer
   const std::uint32_t sw32 = h.sw32;
   constexpr std::uint32_t kBuf = LPT * 4;  // LPT Philox blocks of 4 words
-  const std::uint32_t stride = (2 * sw32 + kBuf + 3) & ~3u;
+  const std::uint32_t nc_words = rp.node_counts ? 8 * sw32 : 0u;  // counter bit-planes
+  const std::uint32_t stride = (2 * sw32 + kBuf + nc_words + 3) & ~3u;
   std::uint32_t* S0 = reinterpret_cast<std::uint32_t*>(smem + staged) +
                       static_cast<std::size_t>(slot) * stride;
   std::uint32_t* S1 = S0 + sw32;
   std::uint32_t* dbuf = S0 + 2 * sw32;  // 16-B aligned: 2*sw32 is a multiple of 4
+  std::uint32_t* planes = dbuf + kBuf;   // node counts: plane i of word w at [8*w + i]
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
     for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w];
+    if (rp.node_counts)
+      for (std::uint32_t w = r; w < sw32; w += LPT)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) planes[8 * w + i] = 0;
   }
   __syncwarp(smask);
+
+  // Per-node one-counts: each lane adds its state words to 8-plane bit-sliced
+  // counters (carry-save, 3 ops per plane) and flushes them to the global u64
+  // counts every 255 steps and at the end.
+  std::uint32_t nc_pending = 0;
+  auto nc_flush = [&]() {
+    std::uint64_t* dst = rp.node_counts + tloc * h.n_kept;
+    for (std::uint32_t w = r; w < sw32; w += LPT) {
+      std::uint32_t pl[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pl[i] = planes[8 * w + i];
+        planes[8 * w + i] = 0;
+      }
+      for (std::uint32_t b = 0; b < 32; ++b) {
+        const std::uint32_t node = 32 * w + b;
+        if (node >= h.n_kept) break;
+        std::uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c |= ((pl[i] >> b) & 1u) << i;
+        if (c) dst[node] += c;
+      }
+    }
+    nc_pending = 0;
+  };
 
   const std::uint32_t k = h.k, g = h.g;
   const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks of phase A = draws 0..g
@@ -470,6 +501,19 @@ __global__ void __launch_bounds__(1024, 1)
       n11 += (prev == 1) & (hit == 1);
       prev = hit;
     }
+    if (rp.node_counts) {  // launch-uniform branch
+      const std::uint32_t* Sf = cur ? S1 : S0;
+      for (std::uint32_t w = r; w < sw32; w += LPT) {
+        std::uint32_t x = Sf[w];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const std::uint32_t p = planes[8 * w + i];
+          planes[8 * w + i] = p ^ x;
+          x &= p;
+        }
+      }
+      if (++nc_pending == 255) nc_flush();
+    }
     if (ser != nullptr && r == 0) {  // launch-uniform branch
       const std::uint64_t pos = rp.series_bit0 + (s - rp.step_begin);
       sword |= hit << (pos & 31);
@@ -481,6 +525,7 @@ __global__ void __launch_bounds__(1024, 1)
     __syncwarp(smask);
   }
   if (rp.tprev && r == 0) rp.tprev[tloc] = static_cast<std::uint8_t>(prev | (kphase << 2));
+  if (rp.node_counts && nc_pending) nc_flush();
 
   {
     const std::uint32_t* Sf = cur ? S1 : S0;
@@ -619,8 +664,8 @@ kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, bool rg) {
                               : pick_lpt<STREAM_U32>(lpt, place, rg);
 }
 
-std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt) {
-  return (2 * h.sw32 + lpt * 4 + 3) & ~3u;
+std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
+  return (2 * h.sw32 + lpt * 4 + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
 }
 
 cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
@@ -636,7 +681,8 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
   std::size_t staged = 0;
   if (place == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
   if (place == PLACE_CORE) staged = h.core_bytes;
-  const std::size_t smem = staged + static_cast<std::size_t>(slots) * slot_words(h, lpt) * 4 + 16;
+  const std::size_t smem =
+      staged + static_cast<std::size_t>(slots) * slot_words(h, lpt, rp.node_counts != nullptr) * 4 + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

@@ -146,3 +146,16 @@ def test_sampled_transitions_and_series_vs_oracle(pb, orc, cuda_ok, kappa, mode)
         assert np.array_equal(st_d, st_o)
         assert np.array_equal(tp_d, tp_o)
     assert np.array_equal(ser_d, ser_o)
+
+
+@pytest.mark.parametrize("case,lpt", [("c1", 0), ("c1", 4), ("c2", 0), ("c3", 8), ("c5", 0)])
+def test_node_one_counts_vs_oracle(pb, orc, cuda_ok, case, lpt):
+    """simulate()'s per-node one-counts (engine.hpp:378-379), incl. >255-step
+    flushes and the plan-placement fallback when the counter planes need room."""
+    plan, pred = _setup(pb, case)
+    eng = pb.GpuEnsemble(plan, lanes_per_traj=lpt)
+    n, steps = (40, 600) if plan.n_kept > 500 else (100, 1000)
+    st, cnt, nc = eng.simulate(seed=8, n_traj=n, n_steps=steps, pred=pred, node_counts=True)
+    ost, ocnt, onc = orc.simulate(plan.view, 8, 0, n, steps, pred=pred, node_counts=True)
+    assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+    assert np.array_equal(nc, onc)
