@@ -122,7 +122,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
                          bool node_counts) {
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
-  w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(32, w));
+  w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? 28 : 32, w));
   const std::uint64_t stride =
       (2 * g.ep.h.sw32 + lpt * 4 + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
