@@ -451,19 +451,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
         }
         __syncwarp(smask);
-        if (DPB == 4 && j0 + 4 * LPT <= A1) {
-          // a full chunk of single-node rounds: four independent chains
-          const std::uint32_t b0 = single_bit(Sc, wreg, j0 + r, r);
-          const std::uint32_t b1 = single_bit(Sc, wreg, j0 + LPT + r, LPT + r);
-          const std::uint32_t b2 = single_bit(Sc, wreg, j0 + 2 * LPT + r, 2 * LPT + r);
-          const std::uint32_t b3 = single_bit(Sc, wreg, j0 + 3 * LPT + r, 3 * LPT + r);
-          store_bits(Sn, j0, __ballot_sync(smask, b0));
-          store_bits(Sn, j0 + LPT, __ballot_sync(smask, b1));
-          store_bits(Sn, j0 + 2 * LPT, __ballot_sync(smask, b2));
-          store_bits(Sn, j0 + 3 * LPT, __ballot_sync(smask, b3));
-          __syncwarp(smask);
-          continue;
-        }
         // rounds are taken in pairs: both rounds' loads are issued before
         // either ballot/store, so the two dependency chains overlap
 #pragma unroll
