@@ -155,6 +155,40 @@ def cpu_reference_rate(text, w, terms, seconds, threads=None):
     return rate, threads, steps, t, rplan.n_kept
 
 
+def reference_estimate_arm(a, w, rplan, terms, threads):
+    """c3 reference arm: the reference's own estimate_steady_state (r = 1e-3,
+    conf 0.95, xoshiro256), one independent estimate per host thread."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(seed):
+        return rplan.estimate(terms, 1e-3, 0.95, 10000, seed, -1, 0)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(9000, 9000 + threads * max(1, a.warmup // 3))))
+    total, steps, est = 0.0, 0, []
+    for k in range(a.steps):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            rs = list(ex.map(one, range(100 * k, 100 * k + threads)))
+        total += time.perf_counter() - t0
+        steps += sum(r["steps"] for r in rs)
+        est.append(rs[0]["estimate"])
+    val = steps * rplan.n_kept / total
+    print(json.dumps({
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1000 * total / a.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": rplan.n_kept,
+                   "precision": 1e-3, "confidence": 0.95},
+        "trajectory_steps_per_s": steps / total, "estimates": est,
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} concurrent reference estimate_steady_state runs "
+                                   f"per step (xoshiro256)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
 def run_reference_arm(a):
     rank, world, local = dist_env()
     if rank != 0:
@@ -168,6 +202,8 @@ def run_reference_arm(a):
     rplan = ref.parse(text).prepare(w.theta, w.k_max, w.mgp)
     pred = rplan.compile_predicate(terms)
     threads = os.cpu_count() or 1
+    if w.n_steps == 0:
+        return reference_estimate_arm(a, w, rplan, terms, threads)
     t, _ = rplan.bench_xoshiro(42, 1, 2000, pred)
     steps = max(1000, int(6.0 / max(t / 2000, 1e-9)))  # ~6 s per bench step
     for _ in range(a.warmup):
@@ -196,12 +232,103 @@ def run_reference_arm(a):
     print(json.dumps(line), flush=True)
 
 
+def run_estimate_mode(a, torch, dist, rank, world, local, dev):
+    """c3: pooled two-state MC steady-state estimate (r = 1e-3, conf 0.95) over
+    the config's trajectories, strong-scaled across ranks (shard_range); the
+    C++ estimator drives per-rank device rounds with one all-reduce of the
+    pooled counters per round. One bench step = one complete estimate."""
+    import paper_1605_00854_b200 as pb
+    from paper_1605_00854_b200.ensemble import DeviceShard, estimate_sharded, shard_range
+
+    w, text, model, plan, terms = build_workload(a.config, a.p)
+    pred = plan.compile_predicate(terms)
+    n_total = a.traj or w.n_traj
+    stream = pb.STREAM_U53 if a.stream == "u53" else pb.STREAM_U32
+    eng = pb.GpuEnsemble(plan, device=local, lanes_per_traj=a.lpt, placement=a.placement)
+    b, c = shard_range(n_total, world, rank)
+    pilot = 1000
+    cap = pilot + 1
+
+    def one(seed):
+        shard = DeviceShard(eng, pred, seed, b, c, stream, cap)
+        req = pb.make_request(precision=1e-3, confidence=0.95, pilot=pilot, seed=seed,
+                              stream=stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = estimate_sharded(req, shard, n_total, cap, device=dev)
+        torch.cuda.synchronize(dev)
+        return time.perf_counter() - t0, res
+
+    for k in range(max(a.warmup, 3)):
+        one(1000 + k)
+    times, results = [], []
+    with ClockSampler(local) as clk:
+        for k in range(a.steps):
+            dt, res = one(42 + k)
+            times.append(dt)
+            results.append(res)
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_s = float(t.item())
+    traj_steps = sum(r["steps_per_traj"] for r in results) * n_total
+    n_kept = plan.n_kept
+    value = traj_steps * n_kept / total_s
+    # end to end through the public C-ABI (pbn_estimate: host states in/out) at N=1
+    e2e = None
+    if world == 1:
+        h_states = np.zeros((n_total, eng.words), np.uint64)
+        t0 = time.perf_counter()
+        e_steps = 0
+        for k in range(a.steps):
+            res, _ = pb.estimate(eng, pred, pb.make_request(
+                precision=1e-3, confidence=0.95, pilot=pilot, seed=42 + k, n_traj=n_total,
+                stream=stream), h_states)
+            e_steps += res["steps_per_traj"] * n_total
+        e2e = {"value": e_steps * n_kept / (time.perf_counter() - t0), "unit": UNIT,
+               "h2d_bytes_per_step": n_total * eng.words * 8,
+               "d2h_bytes_per_step": n_total * eng.words * 8 + 72}
+    if rank != 0:
+        return
+    est = [r["estimate"] for r in results]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": max(a.warmup, 3), "ms_per_step": 1000 * total_s / a.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": n_kept,
+                   "trajectories_total": n_total, "precision": 1e-3, "confidence": 0.95,
+                   "pilot_per_trajectory": pilot, "stream": a.stream,
+                   "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
+                   "engine": eng.info(), "parallelism": f"trajectory-sharded x{world}",
+                   "l2": "inputs (plan + states) re-staged per launch; no flush"},
+        "trajectory_steps_per_s": traj_steps / total_s,
+        "estimates": est, "sample_size_used": [r["sample_size_used"] for r in results],
+        "e2e": e2e, "gpu_launches": None, "clocks": clk.summary(),
+    }
+    if not a.no_cpu_baseline and world == 1:
+        import oracle
+
+        rplan = oracle.Reference().parse(text).prepare(w.theta, w.k_max, w.mgp)
+        t0 = time.perf_counter()
+        r = rplan.estimate(terms, 1e-3, 0.95, 10000, 42, -1, 0)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {
+            "value": r["steps"] * n_kept / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"one reference estimate_steady_state at r=1e-3 ({r['steps']} steps, "
+                      f"{dt:.2f} s, estimate {r['estimate']:.6f})"}
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(a):
     import torch
 
     import paper_1605_00854_b200 as pb
 
     rank, world, local = dist_env()
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
@@ -210,6 +337,11 @@ def run_ours(a):
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if CONFIGS[a.config].n_steps == 0:
+        run_estimate_mode(a, torch, dist if world > 1 else None, rank, world, local, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     w, text, model, plan, terms = build_workload(a.config, a.p)
     flat = plan.flat()

@@ -171,6 +171,8 @@ int pbn_model_generate(const pbn_gen_params* gp, pbn_model** out, uint32_t* pred
 int pbn_model_info(const pbn_model* m, uint32_t* n, double* p, uint32_t* n_interest,
                    double* density);
 int pbn_model_node_index(const pbn_model* m, const char* name, uint32_t* index_out);
+/* Node name i into buf (NUL-terminated, truncated to cap); *len_out = full length. */
+int pbn_model_node_name(const pbn_model* m, uint32_t i, char* buf, size_t cap, size_t* len_out);
 void pbn_model_free(pbn_model* m);
 
 /* ---- preparation (reduction.hpp, perturbation.hpp, grouping.hpp, engine.hpp:85) ---- */
@@ -264,6 +266,9 @@ int pbn_estimate_with_backend(const pbn_estimate_request* req, const pbn_estimat
                               pbn_estimate_result* out);
 int pbn_series_stats_host(const uint32_t* series, uint32_t n_traj, uint64_t stride, uint64_t len,
                           uint32_t kappa, uint64_t* out13);
+/* Same over a DEVICE series buffer (distributed backends all-reduce out13). */
+int pbn_series_stats_device(int device, const uint32_t* d_series, uint32_t n_traj, uint64_t stride,
+                            uint64_t len, uint32_t kappa, uint64_t* out13);
 double pbn_inverse_normal_cdf(double p);
 
 /* ---- test hooks over host internals (grouping.hpp:50-82, alias.hpp:18-56) ---- */

@@ -185,6 +185,7 @@ class Reference:
             "ref_random_small_model": (I, [U64, U32, D, U32, U32, C.POINTER(P)]),
             "ref_alias_build": (I, [PD, U32, PD, PU32]),
             "ref_inverse_normal_cdf": (D, [D]),
+            "ref_last_estimate_steps": (U64, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -349,7 +350,7 @@ class RefPlan:
                                                C.byref(est), C.byref(n), C.byref(burn),
                                                C.byref(deg)))
         return {"estimate": est.value, "sample_size": n.value, "burn_in": burn.value,
-                "degenerate": bool(deg.value)}
+                "degenerate": bool(deg.value), "steps": int(self.ref.lib.ref_last_estimate_steps())}
 
 
 def available():

@@ -36,6 +36,7 @@
 namespace {
 
 thread_local std::string g_err;
+thread_local std::uint64_t g_last_estimate_steps = 0;
 
 template <class F>
 int guarded(F&& f) {
@@ -101,6 +102,19 @@ struct wrapped_stepper {
       ++trans[prev][cur];
       prev = cur;
     }
+  }
+};
+
+// Counts the steps an estimator drives through the reference stepper.
+struct counting_stepper {
+  pbn::grouped_simulator inner;
+  std::uint64_t steps = 0;
+  explicit counting_stepper(const pbn::prepared_simulation& ps) : inner(ps) {}
+  std::uint32_t state_bits() const { return inner.state_bits(); }
+  template <class Rng>
+  void step(pbn::state& s, Rng& rng) {
+    ++steps;
+    inner.step(s, rng);
   }
 };
 
@@ -345,6 +359,8 @@ int ref_bench_xoshiro(void* p, std::uint64_t seed, std::uint32_t n_threads,
   });
 }
 
+std::uint64_t ref_last_estimate_steps() { return g_last_estimate_steps; }
+
 // Reference two-state estimator (estimator.hpp:137-244) on one trajectory.
 // kind < 0: shipped xoshiro256(seed); else the Philox stream of trajectory traj.
 int ref_estimate(void* p, const std::uint32_t* pred_nodes, const std::uint8_t* pred_vals,
@@ -364,14 +380,16 @@ int ref_estimate(void* p, const std::uint32_t* pred_nodes, const std::uint8_t* p
     pbn::state s(ps.kept_count());
     pbn::estimation_result r;
     if (kind < 0) {
-      pbn::grouped_simulator sim(ps);
+      counting_stepper sim(ps);
       pbn::xoshiro256 rng(seed);
       r = pbn::estimate_steady_state(sim, s, cp, req, rng);
+      g_last_estimate_steps = sim.steps;
     } else {
       wrapped_stepper ws(ps);
       philox_rng rng;
       orc_stream_init(&rng.st, seed, traj, kind, ps.pplan.groups);
       r = pbn::estimate_steady_state(ws, s, cp, req, rng);
+      g_last_estimate_steps = rng.next_step;
     }
     *estimate = r.estimate;
     *sample_size = r.sample_size_used;

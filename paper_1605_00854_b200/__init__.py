@@ -150,6 +150,7 @@ def _load():
         "pbn_model_info": (I, [P, C.POINTER(U32), C.POINTER(C.c_double), C.POINTER(U32),
                                C.POINTER(C.c_double)]),
         "pbn_model_node_index": (I, [P, C.c_char_p, C.POINTER(U32)]),
+        "pbn_model_node_name": (I, [P, U32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
         "pbn_model_free": (None, [P]),
         "pbn_prepare": (I, [P, U64, U32, U32, C.POINTER(P)]),
         "pbn_plan_get_view": (I, [P, C.POINTER(PlanView)]),
@@ -176,6 +177,7 @@ def _load():
                                           C.POINTER(EstimateResult)]),
         "pbn_series_stats_host": (I, [C.POINTER(U32), U32, U64, U64, U32, C.POINTER(U64)]),
         "pbn_inverse_normal_cdf": (C.c_double, [C.c_double]),
+        "pbn_series_stats_device": (I, [I, P, U32, U64, U64, U32, C.POINTER(U64)]),
         "pbn_internal_lower_bound": (U32, [C.POINTER(U32), U32, U64]),
         "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
         "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
@@ -191,11 +193,13 @@ def _load():
 lib = _load()
 EXPORTED_SYMBOLS = (
     "pbn_last_error", "pbn_version", "pbn_state_words", "pbn_model_parse", "pbn_model_serialize",
-    "pbn_model_generate", "pbn_model_info", "pbn_model_node_index", "pbn_model_free", "pbn_prepare",
+    "pbn_model_generate", "pbn_model_info", "pbn_model_node_index", "pbn_model_node_name",
+    "pbn_model_free", "pbn_prepare",
     "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
     "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
     "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_destroy", "pbn_estimate",
     "pbn_estimate_with_backend", "pbn_series_stats_host", "pbn_inverse_normal_cdf",
+    "pbn_series_stats_device",
 )
 
 
@@ -246,6 +250,13 @@ class Model:
     @property
     def n(self) -> int:
         return self.info()["n"]
+
+    def node_name(self, i: int) -> str:
+        n = C.c_size_t()
+        _check(lib.pbn_model_node_name(self._h, i, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.pbn_model_node_name(self._h, i, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def node_index(self, name: str) -> int:
         out = C.c_uint32()
@@ -443,6 +454,7 @@ class GpuEnsemble:
         h = C.c_void_p()
         _check(lib.pbn_gpu_create(C.byref(view), device, lanes_per_traj, C.byref(h)))
         self._h = h
+        self._device = device
         if placement != "auto":
             self.set_placement(placement)
 
@@ -510,11 +522,28 @@ class GpuEnsemble:
         return (states, counts, nc) if node_counts else (states, counts)
 
     def simulate_device(self, seed, n_traj, n_steps, d_states, d_counts, traj_begin=0,
-                        step_begin=0, pred=None, stream=STREAM_U53, cuda_stream=0):
+                        step_begin=0, pred=None, stream=STREAM_U53, cuda_stream=0, kappa=1,
+                        thin_mode=0, d_tprev=None, d_series=None, series_stride=0,
+                        series_bit0=0, series_init=False, d_node_counts=None):
         """DEVICE pointers (ints, e.g. torch tensor .data_ptr()), asynchronous."""
         a = self._args(seed, traj_begin, n_traj, n_steps, step_begin, pred, stream)
+        a.kappa, a.thin_mode = kappa, thin_mode
+        if d_tprev is not None:
+            a.tprev = C.cast(C.c_void_p(d_tprev), C.POINTER(C.c_uint8))
+        if d_series is not None:
+            a.series = C.cast(C.c_void_p(d_series), C.POINTER(C.c_uint32))
+            a.series_stride, a.series_bit0 = series_stride, series_bit0
+            a.series_init = 1 if series_init else 0
+        if d_node_counts is not None:
+            a.flags |= RUN_NODE_COUNTS
         _check(lib.pbn_gpu_run_device(self._h, C.byref(a), C.c_void_p(d_states),
-                                      C.c_void_p(d_counts), None, C.c_void_p(cuda_stream)))
+                                      C.c_void_p(d_counts),
+                                      C.c_void_p(d_node_counts) if d_node_counts else None,
+                                      C.c_void_p(cuda_stream)))
+
+    @property
+    def device(self) -> int:
+        return self._device
 
     def last_launches(self) -> int:
         return int(lib.pbn_gpu_last_launches(self._h))
@@ -584,4 +613,31 @@ def series_stats_host(series: np.ndarray, length: int, kappa: int):
     ser = np.ascontiguousarray(series, np.uint32)
     _check(lib.pbn_series_stats_host(_u32p(ser), ser.shape[0], ser.shape[1], length, kappa,
                                      _u64p(out)))
+    return out
+
+
+def stats_csv(plan: "PreparedSimulation", one_counts, steps: int) -> str:
+    """The reference CLI's per-node statistics (pbn_main.cpp:75-85, 207-245):
+    one row per kept node in model order, one_counts in engine order (pooled
+    over trajectories if 2-D), frequency printed with %.12g."""
+    oc = np.asarray(one_counts, dtype=np.uint64)
+    if oc.ndim == 2:
+        oc = oc.sum(axis=0, dtype=np.uint64)
+    red = plan.reduced()
+    rows = ["node,name,one_count,steps,frequency"]
+    for v in range(red["original_n"]):
+        r = int(red["index_map"][v])
+        if r < 0:
+            continue
+        ones = int(oc[int(red["engine_pos"][r])])
+        freq = 0.0 if steps == 0 else ones / steps
+        rows.append(f"{v},{plan.model.node_name(v)},{ones},{steps},{freq:.12g}")
+    return "\n".join(rows) + "\n"
+
+
+def series_stats_device(device: int, d_series: int, n_traj: int, stride: int, length: int,
+                        kappa: int):
+    out = np.zeros(13, np.uint64)
+    _check(lib.pbn_series_stats_device(device, C.c_void_p(d_series), n_traj, stride, length, kappa,
+                                       _u64p(out)))
     return out

@@ -276,6 +276,20 @@ int pbn_model_node_index(const pbn_model* m, const char* name, uint32_t* index_o
   });
 }
 
+int pbn_model_node_name(const pbn_model* m, uint32_t i, char* buf, size_t cap, size_t* len_out) {
+  return guard([&] {
+    need(m, "model");
+    if (i >= m->net.size()) throw model_error("node index out of range");
+    const std::string& nm = m->net.nodes[i].name;
+    if (len_out) *len_out = nm.size();
+    if (buf && cap) {
+      const std::size_t k = std::min(cap - 1, nm.size());
+      std::memcpy(buf, nm.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
 void pbn_model_free(pbn_model* m) { delete m; }
 
 int pbn_prepare(const pbn_model* m, uint64_t theta, uint32_t k_max, uint32_t mgp,
@@ -713,6 +727,20 @@ int pbn_series_stats_host(const uint32_t* series, uint32_t n_traj, uint64_t stri
     need(series, "series");
     need(out13, "out");
     series_stats_host(series, n_traj, stride, len, kappa, out13);
+  });
+}
+
+int pbn_series_stats_device(int device, const uint32_t* d_series, uint32_t n_traj, uint64_t stride,
+                            uint64_t len, uint32_t kappa, uint64_t* out13) {
+  return guard([&] {
+    need(d_series, "series");
+    need(out13, "out");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    dev_buf<unsigned long long> red(13);
+    ck(launch_series_stats(d_series, n_traj, stride, len, kappa, red.p, nullptr), "series stats");
+    unsigned long long t[13];
+    ck(cudaMemcpy(t, red.p, sizeof t, cudaMemcpyDeviceToHost), "D2H");
+    for (int i = 0; i < 13; ++i) out13[i] = t[i];
   });
 }
 

@@ -41,3 +41,76 @@ def run_sharded(simulate, n_total: int, world: int, rank: int, device=None):
     begin, count = shard_range(n_total, world, rank)
     local = pooled(simulate(begin, count)) if count else np.zeros(COUNT_FIELDS, np.int64)
     return allreduce_totals(local, device)
+
+
+# ----------------------------------------------------------------------------
+# Pooled steady-state estimate across ranks ("the estimator does
+# one all-reduce per round"). The C++ estimator (pbn_estimate_with_backend)
+# runs identically on every rank; its backend steps this rank's shard and
+# all-reduces the pooled counters, so every rank takes the same decisions.
+
+class ShardedBackend:
+    """stepper.run(step_begin, n, kappa, thin_mode, series_bit0|None, init) -> local
+    totals (8,); stepper.stats(kappa, length) -> local series counters (13,)."""
+
+    def __init__(self, stepper, device=None):
+        self.stepper, self.device = stepper, device
+
+    def run(self, s0, n, kappa, mode, bit0, init):
+        return allreduce_totals(self.stepper.run(s0, n, kappa, mode, bit0, init), self.device)
+
+    def stats(self, kappa, length):
+        return allreduce_totals(np.asarray(self.stepper.stats(kappa, length), np.int64),
+                                self.device)
+
+
+def estimate_sharded(req, stepper, n_total: int, series_capacity: int, device=None):
+    """Pooled estimate over n_total trajectories split across ranks."""
+    from . import estimate_with_backend
+
+    be = ShardedBackend(stepper, device)
+    req.n_traj = n_total
+    return estimate_with_backend(req, n_total, be.run, be.stats, series_capacity)
+
+
+class DeviceShard:
+    """One rank's trajectory shard on its GPU (torch tensors in HBM)."""
+
+    def __init__(self, engine, pred, seed, traj_begin, n_traj, stream, series_capacity):
+        import torch
+
+        self.eng, self.pred, self.seed = engine, pred, seed
+        self.tb, self.n, self.stream = traj_begin, n_traj, stream
+        dev = torch.device("cuda", engine.device)
+        self.states = torch.zeros((n_traj, engine.words), dtype=torch.int64, device=dev)
+        self.counts = torch.zeros((n_traj, COUNT_FIELDS), dtype=torch.int64, device=dev)
+        self.tprev = torch.zeros(n_traj, dtype=torch.uint8, device=dev)
+        self.stride = (series_capacity + 31) // 32
+        self.series = torch.zeros((n_traj, self.stride), dtype=torch.int32, device=dev)
+        self.cs = torch.cuda.current_stream(dev)
+        self.steps = 0
+
+    def run(self, s0, n, kappa, mode, bit0, init):
+        done = 0
+        tot = np.zeros(COUNT_FIELDS, np.int64)
+        while done < n:
+            m = min(n - done, 1 << 31)
+            self.eng.simulate_device(
+                self.seed, self.n, m, self.states.data_ptr(), self.counts.data_ptr(),
+                traj_begin=self.tb, step_begin=s0 + done, pred=self.pred, stream=self.stream,
+                cuda_stream=self.cs.cuda_stream, kappa=kappa, thin_mode=mode if done == 0 else 1,
+                d_tprev=self.tprev.data_ptr(),
+                d_series=self.series.data_ptr() if bit0 is not None else None,
+                series_stride=self.stride, series_bit0=(bit0 or 0) + done,
+                series_init=init and done == 0)
+            tot += self.counts.sum(dim=0).cpu().numpy()
+            done += m
+        self.steps += n
+        return tot
+
+    def stats(self, kappa, length):
+        from . import series_stats_device
+
+        self.cs.synchronize()
+        return series_stats_device(self.eng.device, self.series.data_ptr(), self.n, self.stride,
+                                   length, kappa).astype(np.int64)

@@ -129,3 +129,25 @@ def test_generator_is_deterministic_and_shaped(pb):
 def test_generator_fixed_targets(pb):
     m, terms = pb.generate_model(100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605)
     assert terms == [(0, 1), (1, 1)]
+
+
+def test_stats_csv_matches_reference_layout(pb, orc, ref):
+    """pbn simulate's CSV (pbn_main.cpp:75-85, 226-235) from one-counts of the
+    reference stepper and of the oracle: identical text."""
+    m = pb.parse_model(CHAIN3_CSV)
+    plan = pb.prepare(m)
+    rplan = ref.parse(CHAIN3_CSV).prepare()
+    _, _, a = rplan.simulate_philox(9, 0, 1, 5000, node_counts=True)
+    _, _, b = orc.simulate(plan.view, 9, 0, 1, 5000, node_counts=True)
+    assert np.array_equal(a, b)
+    csv = pb.stats_csv(plan, b, 5000)
+    lines = csv.splitlines()
+    assert lines[0] == "node,name,one_count,steps,frequency"
+    assert [ln.split(",")[1] for ln in lines[1:]] == ["x0", "x1"]  # x2 is a removed leaf
+    for ln in lines[1:]:
+        v, name, ones, steps, freq = ln.split(",")
+        assert int(steps) == 5000 and freq == "%.12g" % (int(ones) / 5000)
+
+
+CHAIN3_CSV = ("pbn 3\nperturbation 0.05\nnode x0\n  f 1 01 x1\nnode x1\n  f 1 10 x0\n"
+              "node x2\n  f 1 10 x1\ninterest x0 x1\n")

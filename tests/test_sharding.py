@@ -70,3 +70,60 @@ def test_two_rank_gloo_totals_equal_single_process():
     _, cnt = oracle.Oracle().simulate(plan.view, 42, 0, 37, 300, pred=pred)
     want = pooled(cnt).tolist()
     assert res[0] == want and res[1] == want
+
+
+def _est_worker(rank, world, port, out_q):
+    import sys
+
+    import torch.distributed as dist
+
+    import oracle
+    import paper_1605_00854_b200 as pb
+    from paper_1605_00854_b200.ensemble import estimate_sharded
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from estimator_support import OracleEnsemble
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, terms = pb.generate_model(96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607)
+    plan = pb.prepare(model, 1 << 25, 12, 8)
+    pred = plan.compile_predicate(terms)
+    b, c = shard_range(40, world, rank)
+    shard = OracleEnsemble(oracle.Oracle(), plan.view, pred, 3, c, traj_begin=b, cap=4096)
+
+    class Local:
+        def run(self, *a):
+            return shard.run(*a).astype(np.int64)
+
+        def stats(self, kappa, length):
+            return shard.stats(kappa, length)
+
+    res = estimate_sharded(pb.make_request(precision=0.02, pilot=300, seed=3), Local(), 40, 4096)
+    out_q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_estimate_equals_single_process():
+    import oracle
+    import paper_1605_00854_b200 as pb
+    from estimator_support import OracleEnsemble
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_est_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    model, terms = pb.generate_model(96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607)
+    plan = pb.prepare(model, 1 << 25, 12, 8)
+    pred = plan.compile_predicate(terms)
+    single = OracleEnsemble(oracle.Oracle(), plan.view, pred, 3, 40, cap=4096).estimate(
+        pb.make_request(precision=0.02, pilot=300, seed=3, n_traj=40))
+    for k in ("estimate", "sample_size_used", "burn_in_used", "kappa", "steps_per_traj"):
+        assert res[0][k] == res[1][k] == single[k], k
