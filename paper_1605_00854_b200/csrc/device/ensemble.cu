@@ -403,27 +403,30 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     std::uint32_t* Sc = cur ? S1 : S0;
     const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
 
-    // ---- phase A: grouped perturbation + leaf draw (draws 0..g)
+    // ---- phase A: grouped perturbation + leaf draw (draws 0..g). Every draw
+    // of a block is looked up; a per-draw mask keeps full patterns for draws
+    // before the last group, the k'-bit mask for the last group (engine.hpp:
+    // 261) and nothing for the leaf draw and the block's unused tail.
     bool flip = false, leaf = false;
     for (std::uint32_t b = r; b < nb0; b += LPT) {
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+      const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e) {
-        const std::uint32_t d = b * DPB + e;
-        if (d < g) {
-          std::uint32_t c;
-          if constexpr (STREAM == STREAM_U53)
-            c = pert_draw53<GC>(pert53, pick53(x, e), k);
-          else
-            c = pert_draw32<GC>(pert32, pick32(x, e), k);
-          if (d + 1 == g) c &= h.last_mask;
-          if (c != 0) {  // xor_chunk (bitstate.hpp:50-58)
-            flip = true;
-            const std::uint32_t o = d * k, w = o >> 5, sh = o & 31;
-            atomicXor(Sc + w, c << sh);
-            if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
-          }
-        } else if (d == g) {
+        std::uint32_t c;
+        if constexpr (STREAM == STREAM_U53)
+          c = pert_draw53<GC>(pert53, pick53(x, e), k);
+        else
+          c = pert_draw32<GC>(pert32, pick32(x, e), k);
+        const int q = rem - 1 - static_cast<int>(e);
+        c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+        if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+          flip = true;
+          const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
+          atomicXor(Sc + w, c << sh);
+          if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
+        }
+        if (q == -1) {  // this element is the leaf draw (engine.hpp:268)
           if constexpr (STREAM == STREAM_U53)
             leaf = pick53(x, e).value() > h.leaf_thr53;
           else
