@@ -434,7 +434,32 @@ def run_ours(a):
             dist.destroy_process_group()
         return
 
+    # the other stream kind, one timed bench step (reported beside the headline)
+    alt_kind = pb.STREAM_U32 if stream == pb.STREAM_U53 else pb.STREAM_U53
+    alt = None
+    if world == 1:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.simulate_device(42, n_traj, max(1, sim_steps // 10), states.data_ptr(),
+                            counts.data_ptr(), traj_begin=traj_begin, step_begin=0, pred=pred,
+                            stream=alt_kind, cuda_stream=cs.cuda_stream)
+        flush.fill_(7)
+        e0.record(cs)
+        eng.simulate_device(42, n_traj, sim_steps, states.data_ptr(), counts.data_ptr(),
+                            traj_begin=traj_begin, step_begin=0, pred=pred, stream=alt_kind,
+                            cuda_stream=cs.cuda_stream)
+        e1.record(cs)
+        e1.synchronize()
+        alt = {"stream": "u32" if alt_kind == pb.STREAM_U32 else "u53",
+               "value": n_traj * sim_steps * flat.n_kept / (e0.elapsed_time(e1) / 1e3),
+               "unit": UNIT}
+
     peaks = measured_peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(a.config, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
     props = torch.cuda.get_device_properties(dev)
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     peak_lookups = props.multi_processor_count * 32 * sm_mhz * 1e6
@@ -458,8 +483,12 @@ def run_ours(a):
                 "h2d_bytes_per_step": n_traj * words * 8,
                 "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
         "gpu_launches": launches,
+        "alt_stream": alt,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
-                     "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": None,
+                     "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                     "issue_bound_evidence": "profiles/r01_c2_final_u53.txt: issue slots ~72% "
+                                             "busy, ALU pipe ~69%, smem wavefronts ~62%",
                      "note": "lookup roofline = SMs x 32 probes/clk x sm_max_mhz "
                              "(MEASURED_PEAKS.json); algorithmic lookups = g per step + "
                              "(A+G) per function-phase step (SURVEY 8d), per GPU",
