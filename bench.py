@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--placement", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", default="auto", choices=["auto", "simulate", "estimate"],
+                    help="c3 defaults to the steady-state estimate workload")
     return ap.parse_args()
 
 
@@ -337,7 +339,7 @@ def run_ours(a):
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if CONFIGS[a.config].n_steps == 0:
+    if a.mode == "estimate" or (a.mode == "auto" and CONFIGS[a.config].n_steps == 0):
         run_estimate_mode(a, torch, dist if world > 1 else None, rank, world, local, dev)
         if world > 1:
             dist.destroy_process_group()

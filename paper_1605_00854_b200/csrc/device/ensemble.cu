@@ -368,11 +368,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     return (F.x >> v) & 1u;
   };
   // A single-node round's ballot word lands at bit jr of the next state.
-  auto store_bits = [&](std::uint32_t* Sn, std::uint32_t jr, std::uint32_t bits) {
+  // full: all LPT groups of the round exist (a partial last round shares its
+  // word with the next region and must OR atomically).
+  auto store_bits = [&](std::uint32_t* Sn, std::uint32_t jr, std::uint32_t bits, bool full) {
     if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
     if (r == 0 && bits) {
       const std::uint32_t w = jr >> 5, sh = jr & 31;
-      if (LPT == 32) {
+      if (LPT == 32 && full) {
         Sn[w] = bits;  // jr is a multiple of 32: the word is this round's alone
       } else {
         atomicOr(Sn + w, bits << sh);
@@ -463,8 +465,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           if (jr1 + LPT <= A1) {
             const std::uint32_t b0 = single_bit(Sc, wreg, jr0 + r, t * LPT + r);
             const std::uint32_t b1 = single_bit(Sc, wreg, jr1 + r, (t + 1) * LPT + r);
-            store_bits(Sn, jr0, __ballot_sync(smask, b0));
-            store_bits(Sn, jr1, __ballot_sync(smask, b1));
+            store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
+            store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
             continue;
           }
 #pragma unroll
@@ -473,7 +475,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             if (jr >= A) break;
             const std::uint32_t j = jr + r;
             if (jr + LPT <= A1) {
-              store_bits(Sn, jr, __ballot_sync(smask, single_bit(Sc, wreg, j, (t + u) * LPT + r)));
+              store_bits(Sn, jr, __ballot_sync(smask, single_bit(Sc, wreg, j, (t + u) * LPT + r)),
+                         true);
+            } else if (A1 == A) {
+              // partial last round of an all-single-node alias region: lanes
+              // past the region evaluate a valid group and drop the bit
+              const std::uint32_t b = single_bit(Sc, wreg, j < A ? j : A - 1, (t + u) * LPT + r);
+              store_bits(Sn, jr, __ballot_sync(smask, j < A ? b : 0u), false);
             } else {
               const bool act = j < A;
               std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
