@@ -492,13 +492,16 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         }
         __syncwarp(smask);
       }
-      // plain region (one combined function per group, no draw)
-      for (std::uint32_t gr = A; gr < NG; gr += LPT) {
-        const std::uint32_t gi = gr + r;
-        const bool act = gi < NG;
-        std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
-        if (act) eval_group(Sc, gi, 0, olo, ohi, off, members);
-        emit_round(Sn, act, olo, ohi, off, members);
+      // plain region (one combined function per group, no draw), rounds in
+      // pairs: both rounds' loads before either round's atomics
+      for (std::uint32_t gr = A; gr < NG; gr += 2 * LPT) {
+        const std::uint32_t g0 = gr + r, g1 = gr + LPT + r;
+        const bool a0 = g0 < NG, a1 = g1 < NG;
+        std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
+        if (a0) eval_group(Sc, g0, 0, lo0, hi0, off0, m0);
+        if (a1) eval_group(Sc, g1, 0, lo1, hi1, off1, m1);
+        emit_round(Sn, a0, lo0, hi0, off0, m0);
+        if (gr + LPT < NG) emit_round(Sn, a1, lo1, hi1, off1, m1);
       }
       __syncwarp(smask);
       cur ^= 1;
