@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--placement", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--method", default="grouped", choices=["grouped", "reduction", "old"],
+                    help="stepper: the structure-based grouped stepper (the hot path) or the "
+                         "reference's node-by-node Method_reduction / Method_old")
     ap.add_argument("--mode", default="auto", choices=["auto", "simulate", "estimate"],
                     help="c3 defaults to the steady-state estimate workload")
     return ap.parse_args()
@@ -62,7 +65,7 @@ def dist_env():
     return rank, world, local
 
 
-def build_workload(cfg, p_override):
+def build_workload(cfg, p_override, method="grouped"):
     """Model text is the interchange format: both this library and the
     reference parse the same text, so their plans are bitwise identical."""
     import paper_1605_00854_b200 as pb
@@ -71,7 +74,10 @@ def build_workload(cfg, p_override):
     model, terms = w.model(p_override)
     text = model.serialize()
     model = pb.parse_model(text)
-    plan = pb.prepare(model, w.theta, w.k_max, w.mgp)
+    if method == "grouped":
+        plan = pb.prepare(model, w.theta, w.k_max, w.mgp)
+    else:
+        plan = pb.prepare_nodewise(model, method == "reduction")
     return w, text, model, plan, terms
 
 
@@ -138,23 +144,30 @@ def measured_peaks():
         return {}
 
 
-def cpu_reference_rate(text, w, terms, seconds, threads=None):
-    """The unmodified reference grouped stepper (oracle/_ref, xoshiro256),
-    one trajectory per host thread. Returns (traj-steps/s, threads, sample)."""
+METHOD_CODE = {"grouped": 0, "old": 1, "reduction": 2}
+
+
+def cpu_reference_rate(text, w, terms, seconds, threads=None, method="grouped"):
+    """The unmodified reference stepper (oracle/_ref, xoshiro256) — grouped,
+    Method_old or Method_reduction — one trajectory per host thread.
+    Returns (traj-steps/s, threads, steps, seconds, state bits)."""
     import oracle
 
     ref = oracle.Reference()
-    rplan = ref.parse(text).prepare(w.theta, w.k_max, w.mgp)
+    rm = ref.parse(text)
+    rplan = rm.prepare(w.theta, w.k_max, w.mgp)
     pred = rplan.compile_predicate(terms)
     threads = threads or os.cpu_count() or 1
+    code = METHOD_CODE[method]
     # calibrate on one thread, then size the sample to ~`seconds`
     s_cal = 2000
-    t, _ = rplan.bench_xoshiro(42, 1, s_cal, pred)
+    t, _ = rplan.bench_xoshiro(42, 1, s_cal, pred, code)
     per_step = max(t / s_cal, 1e-9)
     steps = max(1000, int(seconds / per_step))
-    t, _ = rplan.bench_xoshiro(42, threads, steps, pred)
+    t, _ = rplan.bench_xoshiro(42, threads, steps, pred, code)
     rate = threads * steps / t
-    return rate, threads, steps, t, rplan.n_kept
+    n_state = {"grouped": rplan.n_kept, "reduction": rplan.n_kept}.get(method, w.n)
+    return rate, threads, steps, t, n_state
 
 
 def reference_estimate_arm(a, w, rplan, terms, threads):
@@ -345,7 +358,7 @@ def run_ours(a):
             dist.destroy_process_group()
         return
 
-    w, text, model, plan, terms = build_workload(a.config, a.p)
+    w, text, model, plan, terms = build_workload(a.config, a.p, a.method)
     flat = plan.flat()
     pred = plan.compile_predicate(terms)
     n_traj = a.traj or w.n_traj
@@ -472,6 +485,7 @@ def run_ours(a):
         "warmup": max(a.warmup, 3), "ms_per_step": total_ms / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": flat.n_kept,
+                   "method": a.method,
                    "trajectories_per_gpu": n_traj, "sim_steps_per_bench_step": sim_steps,
                    "p": a.p if a.p is not None else w.p,
                    "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
@@ -499,11 +513,12 @@ def run_ours(a):
     }
     if not a.no_cpu_baseline and world == 1:
         try:
-            rate, threads, steps, secs, nk = cpu_reference_rate(text, w, terms, a.cpu_seconds)
+            rate, threads, steps, secs, nk = cpu_reference_rate(text, w, terms, a.cpu_seconds,
+                                                                method=a.method)
             line["cpu_baseline"] = {
                 "value": rate * nk, "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"{threads} threads x {steps} steps ({secs:.1f} s), unmodified reference "
-                          f"grouped_simulator + xoshiro256 (oracle/_ref)",
+                          f"{a.method} stepper + xoshiro256 (oracle/_ref)",
                 "trajectory_steps_per_s": rate}
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(e)}

@@ -112,6 +112,17 @@ typedef struct pbn_plan_view {
   const uint32_t* fn_gather;       /* engine bit positions, lists padded to >= 8 with n_kept */
   uint64_t n_table;
   const uint64_t* fn_tables;       /* packed member outputs (member 0 = bit 0)               */
+  /* Stepper kind. Grouped plans (pbn_prepare): pert_mode 0 (g pattern draws
+   * through the 2^k alias cells), has_leaf 1, grp_members NULL (member counts
+   * follow from the offsets). Node-wise plans (pbn_prepare_nodewise, the
+   * reference's Method_old / Method_reduction steppers, engine.hpp:168-242):
+   * pert_mode 1 (g = n per-node Bernoulli(pert_p) draws, flip iff u < p),
+   * has_leaf 0 (Method_old) or 1 (Method_reduction), one group per node at
+   * offset = node index (multi-function nodes first), grp_members all 1. */
+  uint32_t pert_mode;
+  uint32_t has_leaf;
+  double pert_p;
+  const uint32_t* grp_members;     /* [n_groups] or NULL                                     */
 } pbn_plan_view;
 
 /* BASELINE-shaped synthetic network. */
@@ -178,6 +189,10 @@ void pbn_model_free(pbn_model* m);
 /* ---- preparation (reduction.hpp, perturbation.hpp, grouping.hpp, engine.hpp:85) ---- */
 int pbn_prepare(const pbn_model* m, uint64_t theta, uint32_t k_max, uint32_t max_group_parents,
                 pbn_plan** out);
+/* Node-wise plan of the reference's node-by-node steppers: reduced = 0 ->
+ * reference_simulator on the full model (engine.hpp:168-221); reduced = 1 ->
+ * reduced_simulator on the leaf-reduced model (engine.hpp:225-242). */
+int pbn_prepare_nodewise(const pbn_model* m, int reduced, pbn_plan** out);
 int pbn_plan_get_view(const pbn_plan* plan, pbn_plan_view* view); /* valid while plan lives */
 /* Reduction bookkeeping: original n, removed count, index_map[n] (-1 removed),
  * engine_pos[n_kept] (reduced index -> engine bit). Arrays may be NULL. */

@@ -40,6 +40,8 @@ class PlanView(C.Structure):
         ("fn_table_begin", C.POINTER(C.c_uint64)), ("fn_gather_count", C.POINTER(C.c_uint32)),
         ("n_gather", C.c_uint64), ("fn_gather", C.POINTER(C.c_uint32)),
         ("n_table", C.c_uint64), ("fn_tables", C.POINTER(C.c_uint64)),
+        ("pert_mode", C.c_uint32), ("has_leaf", C.c_uint32), ("pert_p", C.c_double),
+        ("grp_members", C.POINTER(C.c_uint32)),
     ]
 
 
@@ -176,6 +178,8 @@ class Reference:
             "ref_simulate_philox": (I, [P, U64, U64, U32, I, U64, U64, PU32, PU8, U32, PU64,
                                         PU64, PU64]),
             "ref_step_scripted": (I, [P, PU64, PD, U32, PU32]),
+            "ref_simulate_nodewise": (I, [P, I, U64, U64, U32, I, U64, U64, PU32, PU8, U32, PU64,
+                                          PU64, PU64]),
             "ref_bench_xoshiro": (I, [P, U64, U32, U64, PU32, PU8, U32, I, P, PD, PU64]),
             "ref_estimate": (I, [P, PU32, PU8, U32, D, D, U64, U64, I, U32, PD, PU64, PU64,
                                  C.POINTER(C.c_int)]),
@@ -242,6 +246,23 @@ class RefModel:
         h = C.c_void_p()
         self.ref._ck(self.ref.lib.ref_prepare(self._h, theta, k_max, mgp, C.byref(h)))
         return RefPlan(self.ref, h, self)
+
+    def simulate_nodewise(self, reduced, n_state, seed, traj_begin, n_traj, n_steps,
+                          states=None, step_begin=0, pred=None, stream=0, node_counts=False):
+        """Method_old (reduced=0) / Method_reduction (1) through pbn::simulate;
+        counts carry steps and hits only."""
+        words = n_state // 64 + 1
+        st = (np.zeros((n_traj, words), np.uint64) if states is None
+              else np.ascontiguousarray(states, np.uint64).copy())
+        counts = np.zeros((n_traj, 8), np.uint64)
+        nc = np.zeros((n_traj, n_state), np.uint64) if node_counts else None
+        bits = np.zeros(1, np.uint32) if pred is None else np.ascontiguousarray(pred[0], np.uint32)
+        vals = np.zeros(1, np.uint8) if pred is None else np.ascontiguousarray(pred[1], np.uint8)
+        npred = 0 if pred is None else len(pred[0])
+        self.ref._ck(self.ref.lib.ref_simulate_nodewise(
+            self._h, reduced, seed, traj_begin, n_traj, stream, step_begin, n_steps, _u32p(bits),
+            _u8p(vals), npred, _u64p(st), _u64p(counts), _u64p(nc) if nc is not None else None))
+        return (st, counts, nc) if node_counts else (st, counts)
 
     def exact_matrix(self, n, t=1.0):
         out = np.zeros((1 << n) * (1 << n), np.float64)

@@ -56,17 +56,26 @@ enum { ORC_PERTURBED = 1, ORC_LEAF = 2, ORC_FN = 3 };
 static int orc_grouped_step(const pbn_plan_view* v, uint64_t* s, uint64_t* next, uint32_t words,
                             orc_stream* rng) {
   int perturbed = 0;
-  for (uint32_t i = 0; i < v->pert_groups; ++i) { /* engine.hpp:257-266 */
-    uint64_t c = orc_alias_draw(orc_stream_next_double(rng), v->pert_size, v->pert_cut,
-                                v->pert_alias);
-    if (i + 1 == v->pert_groups) c &= v->pert_mask;
-    if (c != 0) {
-      orc_xor_chunk(s, c, i * v->pert_k);
-      perturbed = 1;
+  if (v->pert_mode == 1) { /* per-node Bernoulli flips (engine.hpp:190-202) */
+    for (uint32_t i = 0; i < v->pert_groups; ++i)
+      if (orc_stream_next_double(rng) < v->pert_p) {
+        orc_xor_chunk(s, 1, i);
+        perturbed = 1;
+      }
+  } else {
+    for (uint32_t i = 0; i < v->pert_groups; ++i) { /* engine.hpp:257-266 */
+      uint64_t c = orc_alias_draw(orc_stream_next_double(rng), v->pert_size, v->pert_cut,
+                                  v->pert_alias);
+      if (i + 1 == v->pert_groups) c &= v->pert_mask;
+      if (c != 0) {
+        orc_xor_chunk(s, c, i * v->pert_k);
+        perturbed = 1;
+      }
     }
   }
   if (perturbed) return ORC_PERTURBED;                            /* engine.hpp:267 */
-  if (orc_stream_next_double(rng) > v->t) return ORC_LEAF;        /* engine.hpp:268, reduction.hpp:98 */
+  if (v->has_leaf && orc_stream_next_double(rng) > v->t)          /* engine.hpp:268, :237 */
+    return ORC_LEAF;
 
   memset(next, 0, sizeof(uint64_t) * words);                      /* engine.hpp:270 */
   for (uint32_t gi = 0; gi < v->n_groups; ++gi) {
@@ -132,7 +141,8 @@ int orc_simulate_ex(const pbn_plan_view* v, uint64_t seed, uint64_t traj_begin, 
     memset(cnt, 0, sizeof(uint64_t) * PBN_COUNT_FIELDS);
     if (nc) memset(nc, 0, sizeof(uint64_t) * v->n_kept);
     orc_stream rng;
-    orc_stream_init(&rng, seed, (uint32_t)(traj_begin + t), stream_kind, v->pert_groups);
+    orc_stream_init(&rng, seed, (uint32_t)(traj_begin + t), stream_kind,
+                    v->pert_groups + (v->has_leaf ? 1 : 0));
     const int z0 = n_pred ? orc_pred(s, pred_bits, pred_vals, n_pred) : 0;
     int prev = 2;
     uint32_t phase = 0; /* steps since the last sample */
@@ -228,7 +238,7 @@ void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
  * groups, exported for stream tests. */
 double orc_draw(uint64_t seed, uint32_t traj, uint64_t step, uint64_t d, int kind, uint32_t g) {
   orc_stream s;
-  orc_stream_init(&s, seed, traj, kind, g);
+  orc_stream_init(&s, seed, traj, kind, g + 1);
   orc_stream_begin_step(&s, step);
   const uint64_t r = orc_stream_raw(&s, d);
   return kind == 0 ? (double)r * 0x1.0p-53 : (double)r * 0x1.0p-32;

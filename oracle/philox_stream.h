@@ -17,10 +17,11 @@
  *        — the same 53-bit conversion as xoshiro256::next_double (rng.hpp:35)
  *   U32: 4 draws per block, draw e in {0..3}: x[e] * 2^-32
  *   Within a step the draws come in two phases (engine.hpp:255-312):
- *     phase A = draws 0..g (the g grouped-perturbation draws and the leaf draw):
+ *     phase A = the perturbation draws and the leaf draw (g + 1 draws for the
+ *               grouped stepper; n for Method_old, n' + 1 for Method_reduction):
  *               draw d lives in block d / DPB at position d % DPB;
- *     phase B = the function-selection draws of the alias groups, j = d - (g+1):
- *               block NB0 + j / DPB, position j % DPB, NB0 = ceil((g+1) / DPB),
+ *     phase B = the function-selection draws, j = d - g1 (g1 = phase-A draws):
+ *               block NB0 + j / DPB, position j % DPB, NB0 = ceil(g1 / DPB),
  *     i.e. phase B starts on a fresh block, so the device can prefetch its
  *     draws in whole blocks. g is the plan's perturbation group count.
  */
@@ -65,10 +66,12 @@ typedef struct orc_stream {
   uint32_t x[4];
 } orc_stream;
 
+/* g1 = number of phase-A draws per step: g + 1 for the grouped stepper (g
+ * pattern draws + leaf draw), n for Method_old, n' + 1 for Method_reduction. */
 static inline void orc_stream_init(orc_stream* s, uint64_t seed, uint32_t traj, int kind,
-                                   uint32_t g) {
+                                   uint32_t g1) {
   const uint64_t dpb = kind == 0 ? 2 : 4;
-  s->g1 = (uint64_t)g + 1;
+  s->g1 = g1;
   s->nb0 = (s->g1 + dpb - 1) / dpb;
   s->seed = seed;
   s->traj = traj;

@@ -118,6 +118,22 @@ struct counting_stepper {
   }
 };
 
+// Node-by-node stepper with the per-step stream counter (Method_old / Method_reduction).
+struct nodewise_stepper {
+  pbn::reference_simulator* o;
+  pbn::reduced_simulator* r;
+  std::uint32_t bits;
+  std::uint32_t state_bits() const { return bits; }
+  template <class Rng>
+  void step(pbn::state& st, Rng& rng) {
+    orc_stream_begin_step(&rng.st, rng.next_step++);
+    if (r)
+      r->step(st, rng);
+    else
+      o->step(st, rng);
+  }
+};
+
 void fill_view(ref_plan& rp, pbn_plan_view* v) {
   const auto& ps = rp.ps;
   std::memset(v, 0, sizeof *v);
@@ -146,6 +162,8 @@ void fill_view(ref_plan& rp, pbn_plan_view* v) {
   v->fn_gather = ps.fn_gather.data();
   v->n_table = ps.fn_tables.size();
   v->fn_tables = ps.fn_tables.data();
+  v->pert_mode = 0;
+  v->has_leaf = 1;
 }
 
 }  // namespace
@@ -268,7 +286,7 @@ int ref_simulate_philox(void* p, std::uint64_t seed, std::uint64_t traj_begin,
       }
       philox_rng rng;
       orc_stream_init(&rng.st, seed, static_cast<std::uint32_t>(traj_begin + t), kind,
-                      ps.pplan.groups);
+                      ps.pplan.groups + 1);
       rng.next_step = step_begin;
       pbn::sim_options opt;
       opt.count_nodes = node_counts != nullptr;
@@ -284,6 +302,49 @@ int ref_simulate_philox(void* p, std::uint64_t seed, std::uint64_t traj_begin,
       c[PBN_C_T11] = ws.trans[1][1];
       c[PBN_C_FNSTEPS] = ws.fn_steps;
       c[PBN_C_PERTSTEPS] = ws.pert_steps;
+      if (node_counts)
+        std::memcpy(node_counts + static_cast<std::uint64_t>(t) * n, tr.one_counts.data(), 8 * n);
+    }
+  });
+}
+
+// pbn::simulate over the node-by-node steppers on the injected stream:
+// reduced = 0 -> reference_simulator on the full model (engine.hpp:168-221),
+// reduced = 1 -> reduced_simulator on the leaf-reduced model (engine.hpp:225-242).
+// Phase A of the stream = the n (resp. n' + 1 with the leaf draw) first draws.
+int ref_simulate_nodewise(const void* mp, int reduced, std::uint64_t seed,
+                          std::uint64_t traj_begin, std::uint32_t n_traj, int kind,
+                          std::uint64_t step_begin, std::uint64_t n_steps,
+                          const std::uint32_t* pred_bits, const std::uint8_t* pred_vals,
+                          std::uint32_t n_pred, std::uint64_t* states, std::uint64_t* counts,
+                          std::uint64_t* node_counts) {
+  return guarded([&] {
+    const pbn::model& m = *static_cast<const pbn::model*>(mp);
+    const pbn::reduced_model rm = pbn::reduce(m);
+    const std::uint32_t n = reduced ? rm.kept_count() : m.size();
+    const std::uint32_t words = n / 64 + 1;
+    pbn::compiled_predicate cp;
+    for (std::uint32_t i = 0; i < n_pred; ++i) cp.emplace_back(pred_bits[i], pred_vals[i] != 0);
+    pbn::reference_simulator old_sim(m);
+    pbn::reduced_simulator red_sim(rm);
+    for (std::uint32_t t = 0; t < n_traj; ++t) {
+      pbn::state s(n);
+      std::uint64_t* sw = states + static_cast<std::uint64_t>(t) * words;
+      std::memcpy(s.data(), sw, 8 * words);
+      nodewise_stepper w{&old_sim, reduced ? &red_sim : nullptr, n};
+      philox_rng rng;
+      orc_stream_init(&rng.st, seed, static_cast<std::uint32_t>(traj_begin + t), kind,
+                      n + (reduced ? 1 : 0));
+      rng.next_step = step_begin;
+      pbn::sim_options opt;
+      opt.count_nodes = node_counts != nullptr;
+      opt.predicate = n_pred ? &cp : nullptr;
+      const pbn::trajectory tr = pbn::simulate(w, s, n_steps, rng, opt);
+      std::memcpy(sw, s.data(), 8 * words);
+      std::uint64_t* c = counts + static_cast<std::uint64_t>(t) * PBN_COUNT_FIELDS;
+      std::memset(c, 0, 8 * PBN_COUNT_FIELDS);
+      c[PBN_C_STEPS] = tr.steps;
+      c[PBN_C_HITS] = tr.predicate_hits;
       if (node_counts)
         std::memcpy(node_counts + static_cast<std::uint64_t>(t) * n, tr.one_counts.data(), 8 * n);
     }
@@ -334,9 +395,18 @@ int ref_bench_xoshiro(void* p, std::uint64_t seed, std::uint32_t n_threads,
           while (!go.load()) {
           }
           hits[i] = pbn::simulate(sim, s, steps_per_thread, rng, opt).predicate_hits;
-        } else {
+        } else if (method == 1) {
           // Method_old on the full model (engine.hpp:168-221), no predicate mapping
           pbn::reference_simulator sim(*static_cast<const pbn::model*>(model));
+          pbn::state s(sim.state_bits());
+          opt.predicate = nullptr;
+          ready.fetch_add(1);
+          while (!go.load()) {
+          }
+          hits[i] = pbn::simulate(sim, s, steps_per_thread, rng, opt).steps;
+        } else {
+          // Method_reduction (engine.hpp:225-242) on the plan's reduced model
+          pbn::reduced_simulator sim(ps.reduced);
           pbn::state s(sim.state_bits());
           opt.predicate = nullptr;
           ready.fetch_add(1);
@@ -387,7 +457,7 @@ int ref_estimate(void* p, const std::uint32_t* pred_nodes, const std::uint8_t* p
     } else {
       wrapped_stepper ws(ps);
       philox_rng rng;
-      orc_stream_init(&rng.st, seed, traj, kind, ps.pplan.groups);
+      orc_stream_init(&rng.st, seed, traj, kind, ps.pplan.groups + 1);
       r = pbn::estimate_steady_state(ws, s, cp, req, rng);
       g_last_estimate_steps = rng.next_step;
     }

@@ -78,6 +78,8 @@ class PlanView(C.Structure):
         ("fn_table_begin", C.POINTER(C.c_uint64)), ("fn_gather_count", C.POINTER(C.c_uint32)),
         ("n_gather", C.c_uint64), ("fn_gather", C.POINTER(C.c_uint32)),
         ("n_table", C.c_uint64), ("fn_tables", C.POINTER(C.c_uint64)),
+        ("pert_mode", C.c_uint32), ("has_leaf", C.c_uint32), ("pert_p", C.c_double),
+        ("grp_members", C.POINTER(C.c_uint32)),
     ]
 
 
@@ -154,6 +156,7 @@ def _load():
         "pbn_model_free": (None, [P]),
         "pbn_prepare": (I, [P, U64, U32, U32, C.POINTER(P)]),
         "pbn_plan_get_view": (I, [P, C.POINTER(PlanView)]),
+        "pbn_prepare_nodewise": (I, [P, I, C.POINTER(P)]),
         "pbn_plan_reduced": (I, [P, C.POINTER(U32), C.POINTER(U32), C.POINTER(C.c_int32),
                                  C.POINTER(U32), C.POINTER(U32)]),
         "pbn_plan_groups": (I, [P, C.POINTER(U32), C.POINTER(U32)]),
@@ -194,7 +197,7 @@ lib = _load()
 EXPORTED_SYMBOLS = (
     "pbn_last_error", "pbn_version", "pbn_state_words", "pbn_model_parse", "pbn_model_serialize",
     "pbn_model_generate", "pbn_model_info", "pbn_model_node_index", "pbn_model_node_name",
-    "pbn_model_free", "pbn_prepare",
+    "pbn_model_free", "pbn_prepare", "pbn_prepare_nodewise",
     "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
     "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
     "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_destroy", "pbn_estimate",
@@ -425,6 +428,15 @@ def alias_build(probs):
     _check(lib.pbn_internal_alias_build(p.ctypes.data_as(C.POINTER(C.c_double)), len(p),
                                         cut.ctypes.data_as(C.POINTER(C.c_double)), _u32p(al)))
     return cut, al
+
+
+def prepare_nodewise(model: Model, reduced: bool):
+    """Plan of the reference's node-by-node steppers: Method_old
+    (reference_simulator, engine.hpp:168-221) on the full model, or
+    Method_reduction (reduced_simulator, engine.hpp:225-242)."""
+    h = C.c_void_p()
+    _check(lib.pbn_prepare_nodewise(model._h, 1 if reduced else 0, C.byref(h)))
+    return PreparedSimulation(h.value, model, None, None, None)
 
 
 def device_count() -> int:

@@ -303,6 +303,16 @@ int pbn_prepare(const pbn_model* m, uint64_t theta, uint32_t k_max, uint32_t mgp
   });
 }
 
+int pbn_prepare_nodewise(const pbn_model* m, int reduced, pbn_plan** out) {
+  return guard([&] {
+    need(m, "model");
+    need(out, "out");
+    auto p = std::make_unique<pbn_plan>();
+    p->pp = prepare_nodewise_plan(m->net, reduced != 0);
+    *out = p.release();
+  });
+}
+
 int pbn_plan_get_view(const pbn_plan* plan, pbn_plan_view* v) {
   return guard([&] {
     need(plan, "plan");
@@ -334,6 +344,10 @@ int pbn_plan_get_view(const pbn_plan* plan, pbn_plan_view* v) {
     v->fn_gather = pp.fn_gather.data();
     v->n_table = pp.fn_tables.size();
     v->fn_tables = pp.fn_tables.data();
+    v->pert_mode = pp.pert_mode;
+    v->has_leaf = pp.has_leaf;
+    v->pert_p = pp.pert_p;
+    v->grp_members = pp.grp_members.empty() ? nullptr : pp.grp_members.data();
   });
 }
 

@@ -59,6 +59,10 @@ struct dev_plan_header {
                                  // every function's table inline (1 bit x <= 32 entries)
   std::uint32_t rg_ok;           // sw32 <= 32: one state word per lane fits a warp (SHFL gather)
   std::uint32_t single_gc5;      // some function of groups [0, A1) has 5 parents
+  std::uint32_t pert_mode;       // 0 grouped patterns, 1 per-node Bernoulli(p) (Method_old)
+  std::uint32_t has_leaf;        // phase A ends with the leaf draw
+  std::uint64_t pthr53;          // Bernoulli: flip iff r53 < ceil(p * 2^53)
+  std::uint64_t pthr32;          //            flip iff r32 < ceil(p * 2^32)
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   };
 
   const std::uint32_t k = h.k, g = h.g;
-  const std::uint32_t nb0 = (g + 1 + DPB - 1) / DPB;  // blocks of phase A = draws 0..g
+  const std::uint32_t nb0 = (g + h.has_leaf + DPB - 1) / DPB;  // blocks of phase A
   const std::uint32_t A = h.n_alias_groups, NG = h.n_groups, A1 = h.n_single_alias;
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
@@ -410,16 +410,23 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     // before the last group, the k'-bit mask for the last group (engine.hpp:
     // 261) and nothing for the leaf draw and the block's unused tail.
     bool flip = false, leaf = false;
+    const bool bern = h.pert_mode != 0;  // Method_old / Method_reduction plans
     for (std::uint32_t b = r; b < nb0; b += LPT) {
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
       const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e) {
         std::uint32_t c;
-        if constexpr (STREAM == STREAM_U53)
+        if (bern) {  // per-node flip iff u < p (engine.hpp:198)
+          if constexpr (STREAM == STREAM_U53)
+            c = pick53(x, e).value() < h.pthr53 ? 1u : 0u;
+          else
+            c = pick32(x, e) < h.pthr32 ? 1u : 0u;
+        } else if constexpr (STREAM == STREAM_U53) {
           c = pert_draw53<GC>(pert53, pick53(x, e), k);
-        else
+        } else {
           c = pert_draw32<GC>(pert32, pick32(x, e), k);
+        }
         const int q = rem - 1 - static_cast<int>(e);
         c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
         if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
@@ -428,7 +435,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           atomicXor(Sc + w, c << sh);
           if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
         }
-        if (q == -1) {  // this element is the leaf draw (engine.hpp:268)
+        if (q == -1 && h.has_leaf) {  // this element is the leaf draw (engine.hpp:268)
           if constexpr (STREAM == STREAM_U53)
             leaf = pick53(x, e).value() > h.leaf_thr53;
           else

@@ -82,6 +82,16 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.last_mask = static_cast<std::uint32_t>(v.pert_mask);
   h.n_groups = v.n_groups;
   h.rg_ok = h.sw32 <= 32 ? 1u : 0u;
+  if (v.pert_mode > 1) throw model_error("unknown perturbation mode");
+  h.pert_mode = v.pert_mode;
+  h.has_leaf = v.has_leaf ? 1u : 0u;
+  if (v.pert_mode == 1) {
+    if (!(v.pert_p > 0.0 && v.pert_p < 1.0)) throw model_error("perturbation rate must be in (0,1)");
+    if (v.pert_k != 1) throw model_error("Bernoulli perturbation needs k = 1");
+    // u < p  <=>  r < ceil(p * 2^bits)  (p * 2^bits is exact)
+    h.pthr53 = static_cast<std::uint64_t>(std::ceil(std::ldexp(v.pert_p, 53)));
+    h.pthr32 = static_cast<std::uint64_t>(std::ceil(std::ldexp(v.pert_p, 32)));
+  }
   // leaf perturbation iff u > t  <=>  r > floor(t * 2^bits) (t*2^bits is exact)
   const double t53 = std::floor(std::ldexp(v.t, 53));
   h.leaf_thr53 = static_cast<std::uint64_t>(t53);
@@ -129,9 +139,16 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   bool plain_seen = false;
   for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
     const std::uint32_t off = v.grp_offset[gi];
-    const std::uint32_t end = gi + 1 < v.n_groups ? v.grp_offset[gi + 1] : n;
-    if (end <= off || end - off > 64) throw model_error("group member count out of range");
-    const std::uint32_t members = end - off;
+    std::uint32_t members;
+    if (v.grp_members) {
+      members = v.grp_members[gi];
+      if (members == 0 || members > 64 || off + members > n)
+        throw model_error("group member count out of range");
+    } else {
+      const std::uint32_t end = gi + 1 < v.n_groups ? v.grp_offset[gi + 1] : n;
+      if (end <= off || end - off > 64) throw model_error("group member count out of range");
+      members = end - off;
+    }
     const std::uint32_t asz = v.grp_alias_size[gi];
     if (asz >= (1u << 23)) throw resource_error("group alias table too large for the device");
     if (asz == 1) throw model_error("alias table of one cell");

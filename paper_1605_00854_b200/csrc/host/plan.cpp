@@ -397,6 +397,68 @@ std::vector<std::vector<std::uint32_t>> greedy_product_partition(
   return parts;
 }
 
+prepared_plan prepare_nodewise_plan(const network& m, bool reduced) {
+  prepared_plan pp;
+  if (reduced) {
+    reduce_into(m, pp);
+  } else {  // identity "reduction": the full model, t = 1
+    pp.original_n = m.size();
+    pp.kept = m;
+    pp.index_map.resize(m.size());
+    std::iota(pp.index_map.begin(), pp.index_map.end(), 0);
+    pp.t = 1.0;
+  }
+  const network& k = pp.kept;
+  const std::uint32_t n = k.size();
+  if (n == 0) throw model_error("network reduction removed every node");
+  pp.pert_mode = 1;
+  pp.has_leaf = reduced ? 1u : 0u;
+  pp.pert_p = m.p;
+  pp.g = n;  // one Bernoulli draw per node (engine.hpp:194-201)
+  pp.k = 1;
+  pp.k_prime = 1;
+  pp.mask = 1;
+  pp.pert.cut = {1.0, 1.0};
+  pp.pert.alias = {0, 1};
+  // groups: multi-function nodes first (their draws come in node order), then
+  // single-function nodes; every group is one node at its own bit
+  std::vector<std::uint32_t> order;
+  for (std::uint32_t v = 0; v < n; ++v)
+    if (k.nodes[v].nfn() > 1) order.push_back(v);
+  for (std::uint32_t v = 0; v < n; ++v)
+    if (k.nodes[v].nfn() == 1) order.push_back(v);
+  pp.engine_pos.resize(n);
+  pp.engine_nodes.resize(n);
+  for (std::uint32_t v = 0; v < n; ++v) pp.engine_pos[v] = pp.engine_nodes[v] = v;
+  for (auto v : order) {
+    const pbn_node& nd = k.nodes[v];
+    pp.members.push_back({v});
+    pp.grp_members.push_back(1);
+    pp.grp_offset.push_back(v);
+    pp.grp_fn_begin.push_back(static_cast<std::uint32_t>(pp.fn_gather_begin.size()));
+    pp.grp_alias_begin.push_back(static_cast<std::uint32_t>(pp.alias_cut.size()));
+    if (nd.nfn() > 1) {  // selectors_ (engine.hpp:172-177)
+      const walker_table wt = build_walker(nd.probs.data(), nd.probs.size());
+      pp.grp_alias_size.push_back(wt.size());
+      pp.alias_cut.insert(pp.alias_cut.end(), wt.cut.begin(), wt.cut.end());
+      pp.alias_idx.insert(pp.alias_idx.end(), wt.alias.begin(), wt.alias.end());
+    } else {
+      pp.grp_alias_size.push_back(0);
+    }
+    for (const predictor& f : nd.fns) {  // boolean_function::eval (model.hpp:38-43)
+      pp.fn_gather_begin.push_back(pp.fn_gather.size());
+      pp.fn_table_begin.push_back(pp.fn_tables.size());
+      pp.fn_gather_count.push_back(f.arity());
+      for (auto q : f.parents) pp.fn_gather.push_back(q);
+      for (std::size_t b = f.arity(); b < kGatherPad; ++b) pp.fn_gather.push_back(n);
+      for (std::uint64_t x = 0; x < (1ull << f.arity()); ++x)
+        pp.fn_tables.push_back(f.output(x) ? 1ull : 0ull);
+    }
+  }
+  pp.cum.assign(1, 0);
+  return pp;
+}
+
 prepared_plan prepare_plan(const network& m, std::uint64_t theta, std::uint32_t k_max,
                            std::uint32_t max_group_parents) {
   prepared_plan pp;

@@ -57,11 +57,21 @@ struct prepared_plan {
   std::vector<std::uint32_t> fn_gather_count;
   std::vector<std::uint32_t> fn_gather;
   std::vector<std::uint64_t> fn_tables;
+  // stepper kind (see pbn_plan_view): grouped by default
+  std::uint32_t pert_mode = 0, has_leaf = 1;
+  double pert_p = 0.0;
+  std::vector<std::uint32_t> grp_members;  // node-wise plans only
 
   std::uint32_t n_kept() const { return kept.size(); }
 };
 
 prepared_plan prepare_plan(const network& m, std::uint64_t theta, std::uint32_t k_max,
                            std::uint32_t max_group_parents);
+
+// Node-wise plan for the node-by-node steppers (engine.hpp:168-242): one group
+// per node of the full (reduced = false) or leaf-reduced model, per-node alias
+// selectors over the node's functions (alias.hpp:18-56), each function's own
+// parent order as its gather list and its truth table as the table.
+prepared_plan prepare_nodewise_plan(const network& m, bool reduced);
 
 }  // namespace pbn_b200
