@@ -321,7 +321,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // of single-node groups covers consecutive bits: one ballot builds the word.
   auto emit_round = [&](std::uint32_t* Sn, bool act, std::uint32_t olo, std::uint32_t ohi,
                         std::uint32_t off, std::uint32_t members) {
-    const bool single = __all_sync(smask, !act || members == 1);
+    // lane r's group must sit at bit off0 + r (true for grouped plans; node-wise
+    // plans put multi-function nodes first, so their offsets can jump)
+    const std::uint32_t off0 = __shfl_sync(smask, off, (sub * LPT) & 31);
+    const bool single = __all_sync(smask, !act || (members == 1 && off == off0 + r));
     if (single) {
       std::uint32_t bits = __ballot_sync(smask, act && (olo & 1u));
       if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
