@@ -380,6 +380,10 @@ int pbn_compile_predicate(const pbn_plan* plan, const uint32_t* nodes, const uin
                           uint32_t n, uint32_t* bits) {
   return guard([&] {
     need(plan, "plan");
+    if (n) {
+      need(nodes, "nodes");
+      need(bits, "engine_bits_out");
+    }
     const prepared_plan& pp = plan->pp;
     for (uint32_t i = 0; i < n; ++i) {  // engine.hpp:343-362
       if (nodes[i] >= pp.original_n) throw model_error("predicate references a nonexistent node");
@@ -405,10 +409,27 @@ int pbn_device_count(int* count) {
   });
 }
 
+// Every array a view promises must be present (a NULL with a non-zero count
+// would otherwise be dereferenced by the encoder).
+void check_view(const pbn_plan_view& v) {
+  auto req = [](bool ok, const char* what) {
+    if (!ok) throw std::invalid_argument(std::string("plan view: missing ") + what);
+  };
+  req(v.pert_cut && v.pert_alias, "perturbation cells");
+  if (v.n_groups)
+    req(v.grp_offset && v.grp_fn_begin && v.grp_alias_begin && v.grp_alias_size, "group arrays");
+  if (v.n_alias) req(v.alias_cut && v.alias_idx, "alias cells");
+  if (v.n_fns) req(v.fn_gather_begin && v.fn_table_begin && v.fn_gather_count, "function arrays");
+  if (v.n_gather) req(v.fn_gather != nullptr, "gather lists");
+  if (v.n_table) req(v.fn_tables != nullptr, "tables");
+  if (v.n_groups == 0) throw model_error("plan has no groups");
+}
+
 int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu** out) {
   return guard([&] {
     need(view, "view");
     need(out, "out");
+    check_view(*view);
     auto g = std::make_unique<pbn_gpu>();
     g->device = device;
     if (lpt != 0 && (lpt > 32 || (lpt & (lpt - 1)) != 0))

@@ -70,3 +70,27 @@ def test_view_arrays_are_consistent(pb):
     assert int(f.grp_offset[0]) == 0
     assert np.all(f.fn_gather_count <= 30)
     assert f.pert_groups * f.pert_k >= f.n_kept
+
+
+def test_null_arguments_are_errors_not_crashes(pb):
+    import ctypes as C
+
+    lib = pb.lib
+    assert lib.pbn_model_parse(None, 0, C.byref(C.c_void_p())) == 1
+    assert lib.pbn_prepare(None, 1 << 25, 16, 18, C.byref(C.c_void_p())) == 1
+    m, _ = pb.generate_model(20, (1, 2), (1, 2), 0.05, seed=3)
+    plan = pb.prepare(m, 1 << 25, 8, 8)
+    assert lib.pbn_compile_predicate(plan._h, None, None, 2, None) == 1
+    assert lib.pbn_gpu_create(None, 0, 0, C.byref(C.c_void_p())) == 1
+    v = pb.PlanView()
+    v.n_groups = 3  # arrays missing
+    assert lib.pbn_gpu_create(C.byref(v), 0, 0, C.byref(C.c_void_p())) == 1
+    assert b"missing" in lib.pbn_last_error()
+    assert lib.pbn_gpu_create(C.byref(plan.view), 0, 3, C.byref(C.c_void_p())) == 1  # bad LPT
+
+
+def test_inverse_normal_cdf_domain_error_is_reported(pb):
+    f = pb.lib.pbn_inverse_normal_cdf
+    assert abs(f(0.5)) < 1e-12
+    assert f(1.5) != f(1.5)  # NaN outside (0,1), error recorded
+    assert b"normal quantile" in pb.lib.pbn_last_error()
