@@ -480,6 +480,22 @@ def run_ours(a):
     peak_lookups = props.multi_processor_count * 32 * sm_mhz * 1e6
     lookups = flat.expected_lookups(fn_total, traj_steps)
     achieved = lookups / (total_ms / 1e3) / world
+    info = eng.info()
+    lookup_view = {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
+                   "unit": "lookups/s", "frac": achieved / peak_lookups}
+    if info["placement"] == "global":
+        # spill case: every probe is a 32-B sector from L1/L2/HBM
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        ach_gbs = achieved * 32 / 1e9
+        roof = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": ach_gbs / hbm, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                "note": "plan in L1/L2 (placement global): algorithmic bytes = 32 B per table "
+                        "probe (g per step + (A+G) per function-phase step) vs measured HBM copy "
+                        "bandwidth (MEASURED_PEAKS.json)",
+                "lookups_per_step": lookups / traj_steps, "lookup_view": lookup_view}
+    else:
+        roof = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": max(a.warmup, 3), "ms_per_step": total_ms / a.steps, "higher_is_better": True,
@@ -489,7 +505,7 @@ def run_ours(a):
                    "trajectories_per_gpu": n_traj, "sim_steps_per_bench_step": sim_steps,
                    "p": a.p if a.p is not None else w.p,
                    "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
-                   "stream": a.stream, "engine": eng.info(),
+                   "stream": a.stream, "engine": info,
                    "l2": "flushed between timed iterations (256 MiB write)",
                    "parallelism": f"trajectory-sharded x{world}"},
         "trajectory_steps_per_s": traj_steps / (total_ms / 1e3),
@@ -500,7 +516,7 @@ def run_ours(a):
                 "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
         "gpu_launches": launches,
         "alt_stream": alt,
-        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
+        "roofline": roof or {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                      "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                      "issue_bound_evidence": "profiles/r01_c2_final_u53.txt: issue slots ~72% "
