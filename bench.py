@@ -483,19 +483,16 @@ def run_ours(a):
     info = eng.info()
     lookup_view = {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                    "unit": "lookups/s", "frac": achieved / peak_lookups}
+    spill = None
     if info["placement"] == "global":
-        # spill case: every probe is a 32-B sector from L1/L2/HBM
+        # spill case: the plan is read through L1/L2. The lookup
+        # roofline stays the headline; the memory view is reported beside it
+        # (if every probe were a 32-B sector from HBM) — L1 serves ~92% of them
+        # (profiles/r01_c4_u53.txt), so this is an upper bound on memory demand.
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        ach_gbs = achieved * 32 / 1e9
-        roof = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s",
-                "frac": ach_gbs / hbm, "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-                "note": "plan in L1/L2 (placement global): algorithmic bytes = 32 B per table "
-                        "probe (g per step + (A+G) per function-phase step) vs measured HBM copy "
-                        "bandwidth (MEASURED_PEAKS.json)",
-                "lookups_per_step": lookups / traj_steps, "lookup_view": lookup_view}
-    else:
-        roof = None
+        spill = {"bound": "hbm", "algorithmic_gbs_if_every_probe_were_a_sector":
+                 achieved * 32 / 1e9, "peak_gbs": hbm,
+                 "measured": "ncu: L1 hit 92%, L2 hit 99.9%, 459 GB/s L2->SM (profiles/r01_c4_u53.txt)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": max(a.warmup, 3), "ms_per_step": total_ms / a.steps, "higher_is_better": True,
@@ -516,7 +513,8 @@ def run_ours(a):
                 "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
         "gpu_launches": launches,
         "alt_stream": alt,
-        "roofline": roof or {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
+        "spill_view": spill,
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                      "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                      "issue_bound_evidence": "profiles/r01_c2_final_u53.txt: issue slots ~72% "
