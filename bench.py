@@ -481,8 +481,6 @@ def run_ours(a):
     lookups = flat.expected_lookups(fn_total, traj_steps)
     achieved = lookups / (total_ms / 1e3) / world
     info = eng.info()
-    lookup_view = {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
-                   "unit": "lookups/s", "frac": achieved / peak_lookups}
     spill = None
     if info["placement"] == "global":
         # spill case: the plan is read through L1/L2. The lookup
