@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--traj", type=int, default=None, help="trajectories per GPU")
     ap.add_argument("--sim-steps", type=int, default=None, help="simulation steps per bench step")
     ap.add_argument("--lpt", type=int, default=0)
+    ap.add_argument("--k", type=int, default=None, help="override the plan's k_max")
+    ap.add_argument("--mgp", type=int, default=None, help="override max_group_parents")
     ap.add_argument("--placement", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -65,12 +67,18 @@ def dist_env():
     return rank, world, local
 
 
-def build_workload(cfg, p_override, method="grouped"):
+def build_workload(cfg, p_override, method="grouped", k=None, mgp=None):
     """Model text is the interchange format: both this library and the
     reference parse the same text, so their plans are bitwise identical."""
+    import dataclasses
+
     import paper_1605_00854_b200 as pb
 
     w = CONFIGS[cfg]
+    if k is not None:
+        w = dataclasses.replace(w, k_max=k)
+    if mgp is not None:
+        w = dataclasses.replace(w, mgp=mgp)
     model, terms = w.model(p_override)
     text = model.serialize()
     model = pb.parse_model(text)
@@ -210,7 +218,7 @@ def run_reference_arm(a):
         return
     import paper_1605_00854_b200 as pb  # noqa: F401  (model generation / plan only)
 
-    w, text, model, plan, terms = build_workload(a.config, a.p)
+    w, text, model, plan, terms = build_workload(a.config, a.p, "grouped", a.k, a.mgp)
     import oracle
 
     ref = oracle.Reference()
@@ -255,7 +263,7 @@ def run_estimate_mode(a, torch, dist, rank, world, local, dev):
     import paper_1605_00854_b200 as pb
     from paper_1605_00854_b200.ensemble import DeviceShard, estimate_sharded, shard_range
 
-    w, text, model, plan, terms = build_workload(a.config, a.p)
+    w, text, model, plan, terms = build_workload(a.config, a.p, "grouped", a.k, a.mgp)
     pred = plan.compile_predicate(terms)
     n_total = a.traj or w.n_traj
     stream = pb.STREAM_U53 if a.stream == "u53" else pb.STREAM_U32
@@ -358,7 +366,7 @@ def run_ours(a):
             dist.destroy_process_group()
         return
 
-    w, text, model, plan, terms = build_workload(a.config, a.p, a.method)
+    w, text, model, plan, terms = build_workload(a.config, a.p, a.method, a.k, a.mgp)
     flat = plan.flat()
     pred = plan.compile_predicate(terms)
     n_traj = a.traj or w.n_traj

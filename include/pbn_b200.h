@@ -210,8 +210,9 @@ int pbn_device_count(int* count);
 /* Encode + upload a plan. lanes_per_traj: 0 = choose automatically, else 1,2,4,8,16,32. */
 int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lanes_per_traj,
                    pbn_gpu** out);
-/* Force where the plan lives: 0 auto, 1 global (L1/L2), 2 core in smem + tables
- * global, 3 everything in smem. PBN_ERESOURCE if it does not fit. */
+/* Force where the plan lives: 0 auto, 1 global (L1/L2), 2 core in smem, 3 core +
+ * truth tables in smem, 4 everything (incl. perturbation cells) in smem.
+ * PBN_ERESOURCE if it does not fit. */
 int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement);
 int pbn_gpu_info(const pbn_gpu* g, uint32_t* lanes_per_traj, uint32_t* tables_in_smem,
                  uint64_t* smem_bytes, uint64_t* plan_bytes, uint32_t* warps_per_cta);

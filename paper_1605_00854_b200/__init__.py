@@ -476,8 +476,8 @@ class GpuEnsemble:
             self._h = C.c_void_p(None)
 
     def set_placement(self, placement: str) -> None:
-        """'auto' | 'global' | 'core' | 'all' (where the plan lives on the device)."""
-        code = {"auto": 0, "global": 1, "core": 2, "all": 3}[placement]
+        """'auto' | 'global' | 'core' | 'tables' | 'all' (staged prefix of the plan)."""
+        code = {"auto": 0, "global": 1, "core": 2, "tables": 3, "all": 4}[placement]
         _check(lib.pbn_gpu_set_placement(self._h, code))
 
     def info(self):
@@ -485,7 +485,7 @@ class GpuEnsemble:
         sm, pb = C.c_uint64(), C.c_uint64()
         _check(lib.pbn_gpu_info(self._h, C.byref(lpt), C.byref(place), C.byref(sm), C.byref(pb),
                                 C.byref(wpc)))
-        return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "all")[place.value],
+        return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "tables", "all")[place.value],
                 "staged_smem_bytes": sm.value, "plan_bytes": pb.value,
                 "warps_per_cta": wpc.value}
 

@@ -110,11 +110,15 @@ std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t
   return lpt;
 }
 
-std::uint32_t staged_bytes(const pbn_gpu& g) {
-  if (g.place == 2) return g.ep.h.core_bytes + g.ep.h.table_bytes;
-  if (g.place == 1) return g.ep.h.core_bytes;
+// Staged prefix of the blob for a placement level (dev_plan.h); level 3
+// counts both perturbation tables (the launch stages its stream's only).
+std::uint32_t staged_bytes_at(const dev_plan_header& h, int place) {
+  if (place == 3) return h.blob_bytes;
+  if (place == 2) return h.off_pert32;
+  if (place == 1) return h.core_bytes;
   return 0;
 }
+std::uint32_t staged_bytes(const pbn_gpu& g) { return staged_bytes_at(g.ep.h, g.place); }
 
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
@@ -443,12 +447,12 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
     g->smem_optin = static_cast<uint32_t>(optin);
     g->sms = static_cast<uint32_t>(sms);
     const dev_plan_header& h = g->ep.h;
-    if (h.core_bytes + h.table_bytes + kStateReserve <= g->smem_optin)
-      g->place = 2;
-    else if (h.core_bytes + kStateReserve <= g->smem_optin)
-      g->place = 1;
-    else
-      g->place = 0;
+    g->place = 0;
+    for (int lvl = 3; lvl >= 1; --lvl)
+      if (staged_bytes_at(h, lvl) + kStateReserve <= g->smem_optin) {
+        g->place = lvl;
+        break;
+      }
     ck(cudaMalloc(&g->d_blob, g->ep.blob.size()), "cudaMalloc plan");
     ck(cudaMemcpy(g->d_blob, g->ep.blob.data(), g->ep.blob.size(), cudaMemcpyHostToDevice),
        "upload plan");
@@ -459,13 +463,10 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
 int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement) {
   return guard([&] {
     need(g, "gpu");
-    if (placement > 3) throw std::invalid_argument("placement must be 0..3");
+    if (placement > 4) throw std::invalid_argument("placement must be 0..4");
     if (placement == 0) return;
-    const int want = static_cast<int>(placement) - 1;  // 0 global, 1 core, 2 all
-    const dev_plan_header& h = g->ep.h;
-    const std::uint64_t need_bytes = want == 2 ? h.core_bytes + h.table_bytes
-                                     : want == 1 ? h.core_bytes
-                                                 : 0;
+    const int want = static_cast<int>(placement) - 1;  // 0 global, 1 core, 2 +tables, 3 all
+    const std::uint64_t need_bytes = staged_bytes_at(g->ep.h, want);
     if (need_bytes + 4096 > g->smem_optin)
       throw resource_error("requested placement does not fit in shared memory");
     g->place = want;

@@ -2,7 +2,10 @@
 // kernel stages into shared memory with a 1-D bulk copy (cp.async.bulk), plus
 // a small header passed by value as a kernel parameter.
 //
-// Layout (all offsets in bytes from the blob start, each section 16-aligned):
+// Layout (all offsets in bytes from the blob start, each section 16-aligned;
+// order core sections | tables | pert32 | pert53, so every placement level is
+// a prefix: 0 nothing staged, 1 core, 2 core + tables, 3 + perturbation cells
+// of the launch's stream):
 //   pert53[2^k]   u64  perturbation cells for the U53 stream:
 //                      bits [0, 53-k) threshold T, bits [53-k, 53) cell result
 //                      on a miss. A draw r53 picks cell c = r53 >> (53-k) and
@@ -52,7 +55,8 @@ struct dev_plan_header {
   std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
   std::uint32_t off_acut, off_aidx, off_a32, off_arec, off_tables;
   std::uint32_t core_bytes;   // bytes [0, off_tables)
-  std::uint32_t table_bytes;  // bytes [off_tables, off_tables + table_bytes)
+  std::uint32_t table_bytes;  // bytes [off_tables, off_pert32)
+  std::uint32_t blob_bytes;   // whole blob: core | tables | pert32 | pert53
   std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
   std::uint32_t n_alias_groups;  // A: groups [0, A) draw a combined function
   std::uint32_t n_single_alias;  // A1 <= A: groups [0, A1) are single nodes at offset = index,

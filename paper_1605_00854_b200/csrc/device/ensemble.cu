@@ -30,9 +30,18 @@
 namespace pbn_b200 {
 
 enum { STREAM_U53 = 0, STREAM_U32 = 1 };
-// Plan placement: 2 = whole blob in smem, 1 = core in smem + tables in global,
-// 0 = everything in global (read through the read-only L1/L2 path).
-enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_ALL = 2 };
+// Plan placement = the staged prefix of the blob (dev_plan.h): 0 nothing (all
+// reads through the read-only L1/L2 path), 1 core, 2 core + tables, 3 also the
+// perturbation cells of the launch's stream.
+enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_TABLES = 2, PLACE_ALL = 3 };
+
+template <int STREAM>
+__host__ __device__ inline std::uint32_t staged_prefix(const dev_plan_header& h, int place) {
+  if (place == PLACE_ALL) return STREAM == 0 ? h.blob_bytes : h.off_pert53;
+  if (place == PLACE_TABLES) return h.off_pert32;
+  if (place == PLACE_CORE) return h.core_bytes;
+  return 0;
+}
 
 template <bool G, class T>
 __device__ __forceinline__ T ldp(const T* p) {
@@ -155,19 +164,19 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                         std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
-  constexpr bool GC = PLACE == PLACE_GLOBAL;  // core sections read from global
-  constexpr bool GT = PLACE != PLACE_ALL;     // tables read from global
+  constexpr bool GC = PLACE < PLACE_CORE;    // core sections read from global
+  constexpr bool GT = PLACE < PLACE_TABLES;   // tables read from global
+  constexpr bool GP = PLACE < PLACE_ALL;      // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
 
-  std::uint32_t staged = 0;
-  if constexpr (PLACE == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
-  if constexpr (PLACE == PLACE_CORE) staged = h.core_bytes;
+  const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
   if (staged) stage_plan(smem, gblob, staged, &stage_bar);
 
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
-  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(core + h.off_pert53);
-  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(core + h.off_pert32);
+  const std::uint8_t* pbase = GP ? gblob : smem;
+  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pbase + h.off_pert53);
+  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pbase + h.off_pert32);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
@@ -426,9 +435,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           else
             c = pick32(x, e) < h.pthr32 ? 1u : 0u;
         } else if constexpr (STREAM == STREAM_U53) {
-          c = pert_draw53<GC>(pert53, pick53(x, e), k);
+          c = pert_draw53<GP>(pert53, pick53(x, e), k);
         } else {
-          c = pert_draw32<GC>(pert32, pick32(x, e), k);
+          c = pert_draw32<GP>(pert32, pick32(x, e), k);
         }
         const int q = rem - 1 - static_cast<int>(e);
         c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
@@ -662,6 +671,8 @@ kernel_fn pick_place(int place) {
   switch (place) {
     case PLACE_ALL:
       return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, RG>;
+    case PLACE_TABLES:
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, RG>;
     case PLACE_CORE:
       return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, RG>;
     default:
@@ -706,9 +717,8 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;
-  std::size_t staged = 0;
-  if (place == PLACE_ALL) staged = h.core_bytes + h.table_bytes;
-  if (place == PLACE_CORE) staged = h.core_bytes;
+  const std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
+                                                      : staged_prefix<STREAM_U32>(h, place);
   const std::size_t smem =
       staged + static_cast<std::size_t>(slots) * slot_words(h, lpt, rp.node_counts != nullptr) * 4 + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),

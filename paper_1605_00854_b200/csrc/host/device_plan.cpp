@@ -268,8 +268,8 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     off = align16(off + bytes);
     return static_cast<std::uint32_t>(o);
   };
-  h.off_pert53 = section(8 * pert53.size());
-  h.off_pert32 = section(4 * pert32.size());
+  // placement prefixes: [core | tables | pert32 | pert53] — a launch stages
+  // the longest prefix that fits in shared memory and reads the rest via L1/L2
   h.off_groups = section(4 * groups.size());
   h.off_fns = section(4 * fns.size());
   h.off_grec = section(2 * grec.size());
@@ -278,10 +278,13 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.off_a32 = section(4 * a32.size());
   h.off_arec = section(4 * arec.size());
   h.core_bytes = static_cast<std::uint32_t>(off);
-  h.off_tables = static_cast<std::uint32_t>(off);
-  h.table_bytes = static_cast<std::uint32_t>(align16(tables.size()));
-  if (off + h.table_bytes > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
-  ep.blob.assign(off + h.table_bytes, 0);
+  h.off_tables = section(tables.size());
+  h.table_bytes = static_cast<std::uint32_t>(off) - h.off_tables;
+  h.off_pert32 = section(4 * pert32.size());
+  h.off_pert53 = section(8 * pert53.size());
+  h.blob_bytes = static_cast<std::uint32_t>(off);
+  if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
+  ep.blob.assign(off, 0);
   put(ep.blob, h.off_pert53, pert53);
   put(ep.blob, h.off_pert32, pert32);
   put(ep.blob, h.off_groups, groups);

@@ -60,13 +60,14 @@ def test_lanes_per_trajectory_invariance(pb, orc, cuda_ok, lpt):
     assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
 
 
-@pytest.mark.parametrize("placement", ["global", "core", "all"])
+@pytest.mark.parametrize("placement", ["global", "core", "tables", "all"])
 def test_placement_invariance(pb, orc, cuda_ok, placement):
     plan, pred = _setup(pb, "c2")
     eng = pb.GpuEnsemble(plan, placement=placement)
-    st, cnt = eng.simulate(seed=9, n_traj=64, n_steps=300, pred=pred, stream=1)
-    ost, ocnt = orc.simulate(plan.view, 9, 0, 64, 300, pred=pred, stream=1)
-    assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+    for stream in (0, 1):
+        st, cnt = eng.simulate(seed=9, n_traj=64, n_steps=300, pred=pred, stream=stream)
+        ost, ocnt = orc.simulate(plan.view, 9, 0, 64, 300, pred=pred, stream=stream)
+        assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
 
 
 def test_resume_and_shard_invariance(pb, cuda_ok):
