@@ -69,6 +69,8 @@ extern "C" {
 
 /* Run flags. */
 #define PBN_RUN_NODE_COUNTS 1u /* also accumulate per-bit one-counts (engine.hpp:378-379) */
+#define PBN_RUN_EXACT_ALIAS 2u /* U53: every combined-function choice in FP64 (no integer fast
+                                  path); same results, for cross-checking the fast path */
 
 /* Opaque handles. */
 typedef struct pbn_model pbn_model; /* parsed + validated model           (model.hpp:57-69)  */
@@ -291,6 +293,12 @@ double pbn_inverse_normal_cdf(double p);
 uint32_t pbn_internal_lower_bound(const uint32_t* w, uint32_t n, uint64_t theta);
 int pbn_internal_greedy_partition(const uint32_t* w, uint32_t n, uint32_t m, uint32_t* part_of);
 int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint32_t* alias);
+/* Integer form of the U53 combined-function choice (dev_plan.h a53) evaluated on
+ * the host exactly as the kernel does it, fast path and boundary fallback, for
+ * raw draw words R[i] = x[2e+1] << 32 | x[2e]; n <= 2048. Test hook. */
+int pbn_internal_alias53_pick(const double* cut, const uint32_t* alias, uint32_t n,
+                              const uint64_t* raw, uint64_t m, uint32_t* pick,
+                              uint8_t* took_fast);
 
 #ifdef __cplusplus
 }

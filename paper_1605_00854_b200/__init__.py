@@ -28,11 +28,14 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbn_b200.so")
+# PBN_B200_LIB selects an alternative in-tree build (A/B measurements of
+# compile-time variants, see Makefile `variant`)
+LIB_PATH = os.environ.get("PBN_B200_LIB") or os.path.join(_HERE, "libpbn_b200.so")
 
 STREAM_U53 = 0
 STREAM_U32 = 1
 RUN_NODE_COUNTS = 1
+RUN_EXACT_ALIAS = 2
 COUNT_FIELDS = 8
 C_STEPS, C_HITS, C_T00, C_T01, C_T10, C_T11, C_FNSTEPS, C_PERTSTEPS = range(8)
 DEFAULT_THETA = 1 << 25  # engine.hpp:81
@@ -185,6 +188,9 @@ def _load():
         "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
         "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
                                          C.POINTER(U32)]),
+        "pbn_internal_alias53_pick": (I, [C.POINTER(C.c_double), C.POINTER(U32), U32,
+                                          C.POINTER(U64), U64, C.POINTER(U32),
+                                          C.POINTER(C.c_uint8)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -430,6 +436,20 @@ def alias_build(probs):
     return cut, al
 
 
+def alias53_pick(cut, alias, raw):
+    """Test hook: the kernel's integer U53 combined-function choice (dev_plan.h
+    a53) on raw draw words; returns (picks, took_fast_path)."""
+    cut = np.ascontiguousarray(cut, np.float64)
+    alias = np.ascontiguousarray(alias, np.uint32)
+    raw = np.ascontiguousarray(raw, np.uint64)
+    pick = np.zeros(len(raw), np.uint32)
+    fast = np.zeros(len(raw), np.uint8)
+    _check(lib.pbn_internal_alias53_pick(cut.ctypes.data_as(C.POINTER(C.c_double)), _u32p(alias),
+                                         len(cut), _u64p(raw), len(raw), _u32p(pick),
+                                         fast.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return pick, fast.astype(bool)
+
+
 def prepare_nodewise(model: Model, reduced: bool):
     """Plan of the reference's node-by-node steppers: Method_old
     (reference_simulator, engine.hpp:168-221) on the full model, or
@@ -504,11 +524,13 @@ class GpuEnsemble:
 
     def simulate(self, seed, n_traj, n_steps, traj_begin=0, step_begin=0, states=None,
                  pred=None, stream=STREAM_U53, kappa=1, thin_mode=0, tprev=None, series=None,
-                 series_bit0=0, series_init=False, node_counts=False):
+                 series_bit0=0, series_init=False, node_counts=False, exact_alias=False):
         """HOST buffers in/out. states: (n_traj, words) uint64 engine-order (zeros if None).
         pred: (engine bits, values) from PreparedSimulation.compile_predicate.
         kappa/thin_mode/tprev: sampled predicate transitions (see pbn_run_args);
         series: (n_traj, stride) uint32 bit rows updated in place.
+        exact_alias: every U53 combined-function choice takes the FP64 path
+        (checks the integer fast path against it; same results, slower).
         Returns (states, counts[n_traj, 8])."""
         if states is None:
             states = np.zeros((n_traj, self.words), np.uint64)
@@ -525,6 +547,8 @@ class GpuEnsemble:
             a.series = _u32p(series)
             a.series_stride = series.shape[1]
             a.series_bit0, a.series_init = series_bit0, 1 if series_init else 0
+        if exact_alias:
+            a.flags |= RUN_EXACT_ALIAS
         nc = None
         if node_counts:
             a.flags |= RUN_NODE_COUNTS

@@ -128,7 +128,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? 28 : 32, w));
   const std::uint64_t stride =
-      (2 * g.ep.h.sw32 + lpt * 4 + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
+      (2 * g.ep.h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
   const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
   while (w > 1 && w * per_warp > avail) --w;
@@ -143,6 +143,9 @@ dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
   rp.n_traj = a.n_traj;
   rp.step_begin = a.step_begin;
   rp.n_steps = a.n_steps;
+  if (a.flags & ~(PBN_RUN_NODE_COUNTS | PBN_RUN_EXACT_ALIAS))
+    throw std::invalid_argument("unknown run flags");
+  rp.exact_alias = (a.flags & PBN_RUN_EXACT_ALIAS) ? 1u : 0u;
   if (a.n_pred) {
     need(a.pred_bits, "pred_bits");
     need(a.pred_vals, "pred_vals");
@@ -604,6 +607,31 @@ int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint3
     const walker_table t = build_walker(probs, n);
     std::copy(t.cut.begin(), t.cut.end(), cut);
     std::copy(t.alias.begin(), t.alias.end(), alias);
+  });
+}
+
+int pbn_internal_alias53_pick(const double* cut, const uint32_t* alias, uint32_t n,
+                              const uint64_t* raw, uint64_t m, uint32_t* pick,
+                              uint8_t* took_fast) {
+  return guard([&] {
+    need(cut, "cut");
+    need(alias, "alias");
+    need(raw, "raw");
+    need(pick, "pick");
+    if (n < 2 || n > kA53MaxCells) throw std::invalid_argument("n must be in [2, 2048]");
+    const std::vector<std::uint32_t> rec = alias53_records(cut, alias, n);
+    for (uint64_t i = 0; i < m; ++i) {
+      const std::uint64_t R = raw[i];
+      bool rare = false;
+      pick[i] = alias53_pick_int(rec.data(), n, static_cast<std::uint32_t>(R >> 32), rare);
+      const bool fast = !rare;
+      if (rare) {
+        const std::uint64_t r53 = R >> 11;
+        const std::uint32_t c = alias53_cell(r53, n);
+        pick[i] = alias53_frac(r53, n) < cut[c] ? c : alias[c];
+      }
+      if (took_fast) took_fast[i] = fast ? 1 : 0;
+    }
   });
 }
 

@@ -3,16 +3,20 @@
 // a small header passed by value as a kernel parameter.
 //
 // Layout (all offsets in bytes from the blob start, each section 16-aligned;
-// order core sections | tables | pert32 | pert53, so every placement level is
-// a prefix: 0 nothing staged, 1 core, 2 core + tables, 3 + perturbation cells
-// of the launch's stream):
-//   pert53[2^k]   u64  perturbation cells for the U53 stream:
-//                      bits [0, 53-k) threshold T, bits [53-k, 53) cell result
-//                      on a miss. A draw r53 picks cell c = r53 >> (53-k) and
-//                      returns (r53 & (2^(53-k)-1)) < T ? c : alias — exactly
-//                      alias_table::next (alias.hpp:70-76) for N = 2^k, where
-//                      T = ceil(cut * 2^(53-k)); cells whose cut rounds to the
-//                      whole range store (T=0, alias=c).
+// order core sections | tables | pert32 | pert53 | exact, so every placement
+// level is a prefix: 0 nothing staged, 1 core, 2 core + tables, 3 +
+// perturbation cells of the launch's stream; `exact` is never staged):
+//
+// U53 draws are compared in raw-word form: the two Philox words of a draw,
+// R = x[2e+1] << 32 | x[2e], satisfy r53 = R >> 11, so r53 < T  <=>  R < T << 11.
+//
+//   pert53[2^k]   u64  perturbation cells for the U53 stream, raw-word form:
+//                      bits [11, 64-k) threshold T, bits [64-k, 64) cell result
+//                      on a miss. A draw picks cell c = R >> (64-k) and returns
+//                      (R mod 2^(64-k)) < (cell mod 2^(64-k)) ? c : alias —
+//                      exactly alias_table::next (alias.hpp:70-76) for N = 2^k,
+//                      where T = ceil(cut * 2^(53-k)); cells whose cut rounds to
+//                      the whole range store (T=0, alias=c).
 //   pert32[2^k]   u32  the same for the U32 stream with 32-k threshold bits.
 //   groups[G]     uint4 {offset, fn_begin, alias_begin, alias_size | (members-1)<<24};
 //                      the A alias groups come first (grouping.hpp: multi-function
@@ -27,12 +31,22 @@
 //                      (word32 << 5) | ((bit32 - slot) & 31): a funnel rotate by the
 //                      low 5 bits lands the parent bit at `slot`. Unused slots hold
 //                      the always-zero bit n' (engine.hpp:149-150).
-//   acut[A]       f64  group alias cut-offs (U53 path, FP64 like engine.hpp:285-290)
-//   aidx[A]       u32  group alias targets
+//   a53[A]        uint2 U53 combined-function cells, integer form of engine.hpp:
+//                      285-290 for groups of N <= 2048 functions: {alias[c], hi32 of
+//                      C[c]}, C[c] = the first r53 of cell c whose fraction reaches
+//                      cut[c] (alias53_cut_points; capped at 2^53-1). From the draw's
+//                      high word hi: P = hi * N, e = P >> 32. Unless (P mod 2^32) > ~N
+//                      (hi is the last high word of bucket e, where the double
+//                      rounding can cross into cell e+1; N < 2^21 keeps it within one
+//                      step) or hi == hi32(C[e]), the choice is hi < hi32(C[e]) ? e :
+//                      alias[e]; the rare rest (about N+1 draws in 2^32) takes the
+//                      exact FP64 path.
 //   a32[A]        uint2 {ceil(cut * 2^32) or 0, alias or self}: U32 integer path
 //   arec[A1]      u32  compact record of the leading single-node alias groups:
 //                      base | alias_size << 24 (their fn_begin == alias_begin == base)
 //   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
+//   acut[A] f64, aidx[A] u32 (exact section): the group cut-offs and targets
+//                      for the FP64 path (boundary draws, groups with N > 2048)
 #pragma once
 
 #include <cstdint>
@@ -40,6 +54,20 @@
 namespace pbn_b200 {
 
 inline constexpr std::uint32_t kMaxPredWords = 16;
+#ifndef PBN_CHUNK_BLOCKS
+#define PBN_CHUNK_BLOCKS 1
+#endif
+// Phase-B Philox blocks each lane computes per draw-buffer chunk (a chunk is
+// LPT * kChunkBlocks blocks); the per-trajectory draw buffer holds one chunk.
+inline constexpr std::uint32_t kChunkBlocks = PBN_CHUNK_BLOCKS;
+#ifndef PBN_PHILOX_PIPELINE
+#define PBN_PHILOX_PIPELINE 0
+#endif
+// 1: the next chunk's Philox blocks are computed while the current chunk's
+// rounds run (software pipelining; ALU work overlaps the rounds' load latency)
+inline constexpr bool kPhiloxPipeline = PBN_PHILOX_PIPELINE != 0;
+inline constexpr std::uint32_t kA53MaxCells = 2048;           // alias fits the low 11 bits
+inline constexpr std::uint32_t kGroupExactAlias = 1u << 23;   // groups[].w flag: FP64 path only
 
 struct dev_plan_header {
   std::uint32_t n_kept;
@@ -49,14 +77,14 @@ struct dev_plan_header {
   std::uint32_t last_mask;  // 2^k' - 1 (k' <= 24)
   std::uint32_t n_groups;
   std::uint32_t max_alias;  // largest group alias table
-  std::uint64_t leaf_thr53; // floor(t * 2^53): leaf perturbation iff r53 > thr
+  std::uint64_t leaf_thr53; // raw word: leaf perturbation iff R > floor(t * 2^53) << 11 | 0x7FF
   std::uint32_t leaf_thr32; // floor(t * 2^32) (saturated)
   std::uint32_t leaf_never; // t == 1: the leaf draw can never fire
   std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
-  std::uint32_t off_acut, off_aidx, off_a32, off_arec, off_tables;
+  std::uint32_t off_acut, off_aidx, off_a53, off_a32, off_arec, off_tables;
   std::uint32_t core_bytes;   // bytes [0, off_tables)
   std::uint32_t table_bytes;  // bytes [off_tables, off_pert32)
-  std::uint32_t blob_bytes;   // whole blob: core | tables | pert32 | pert53
+  std::uint32_t blob_bytes;   // stageable prefix: core | tables | pert32 | pert53
   std::uint32_t u32_ok;       // every group alias size <= 2^21 (U32 path exact)
   std::uint32_t n_alias_groups;  // A: groups [0, A) draw a combined function
   std::uint32_t n_single_alias;  // A1 <= A: groups [0, A1) are single nodes at offset = index,
@@ -65,7 +93,7 @@ struct dev_plan_header {
   std::uint32_t single_gc5;      // some function of groups [0, A1) has 5 parents
   std::uint32_t pert_mode;       // 0 grouped patterns, 1 per-node Bernoulli(p) (Method_old)
   std::uint32_t has_leaf;        // phase A ends with the leaf draw
-  std::uint64_t pthr53;          // Bernoulli: flip iff r53 < ceil(p * 2^53)
+  std::uint64_t pthr53;          // Bernoulli: flip iff R < ceil(p * 2^53) << 11 (raw word)
   std::uint64_t pthr32;          //            flip iff r32 < ceil(p * 2^32)
 };
 
@@ -82,7 +110,7 @@ struct dev_run_params {
   std::uint32_t rk0[10], rk1[10];  // Philox round keys of the seed
   std::uint64_t traj_begin;
   std::uint32_t n_traj;
-  std::uint32_t pad0;
+  std::uint32_t exact_alias;  // 1: every U53 combined-function choice takes the FP64 path
   std::uint64_t step_begin;
   std::uint64_t n_steps;
   dev_predicate pred;

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "dev_plan.h"
 #include "philox.cuh"
@@ -99,6 +100,10 @@ struct raw53 {
   __device__ __forceinline__ std::uint64_t value() const {
     return (static_cast<std::uint64_t>(hi) << 21) | (lo >> 11);
   }
+  // raw word R = hi << 32 | lo; r53 = R >> 11 (dev_plan.h: raw-word thresholds)
+  __device__ __forceinline__ std::uint64_t raw() const {
+    return (static_cast<std::uint64_t>(hi) << 32) | lo;
+  }
 };
 
 __device__ __forceinline__ raw53 pick53(const uint4& x, std::uint32_t e) {
@@ -108,16 +113,19 @@ __device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e)
   return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
 }
 
-// Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form.
+// Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form on
+// the raw draw word: the cell index is the top k bits, the threshold compare
+// runs on the remaining 64-k bits (dev_plan.h pert53).
 template <bool G>
 __device__ __forceinline__ std::uint32_t pert_draw53(const std::uint64_t* cells, raw53 r,
                                                      std::uint32_t k) {
   const std::uint32_t c = r.hi >> (32 - k);
-  const std::uint32_t lbits = 53 - k;
-  const std::uint64_t lmask = (1ull << lbits) - 1;
-  const std::uint64_t low = r.value() & lmask;
+  const std::uint32_t hmask = 0xFFFFFFFFu >> k;
   const std::uint64_t e = ldp<G>(cells + c);
-  return low < (e & lmask) ? c : static_cast<std::uint32_t>(e >> lbits);
+  const std::uint32_t ehi = static_cast<std::uint32_t>(e >> 32);
+  const std::uint64_t rl = (static_cast<std::uint64_t>(r.hi & hmask) << 32) | r.lo;
+  const std::uint64_t el = (static_cast<std::uint64_t>(ehi & hmask) << 32) | static_cast<std::uint32_t>(e);
+  return rl < el ? c : (ehi >> (32 - k));
 }
 
 template <bool G>
@@ -180,8 +188,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
-  const double* acut = reinterpret_cast<const double*>(core + h.off_acut);
-  const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(core + h.off_aidx);
+  // FP64 cut-offs of the exact path: never staged (dev_plan.h)
+  const double* acut = reinterpret_cast<const double*>(gblob + h.off_acut);
+  const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(gblob + h.off_aidx);
+  const uint2* a53 = reinterpret_cast<const uint2*>(core + h.off_a53);
   const uint2* a32 = reinterpret_cast<const uint2*>(core + h.off_a32);
   const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
 
@@ -197,7 +207,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
 
   // per-trajectory shared memory: two state buffers + the phase-B draw buffer
   const std::uint32_t sw32 = h.sw32;
-  constexpr std::uint32_t kBuf = LPT * 4;  // LPT Philox blocks of 4 words
+  constexpr std::uint32_t CB = kChunkBlocks;
+  constexpr std::uint32_t kBuf = LPT * 4 * CB;  // one chunk of Philox blocks (4 words)
   const std::uint32_t nc_words = rp.node_counts ? 8 * sw32 : 0u;  // counter bit-planes
   const std::uint32_t stride = (2 * sw32 + kBuf + nc_words + 3) & ~3u;
   std::uint32_t* S0 = reinterpret_cast<std::uint32_t*>(smem + staged) +
@@ -241,35 +252,41 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   };
 
   const std::uint32_t k = h.k, g = h.g;
+  const bool exact_all = rp.exact_alias != 0;
   const std::uint32_t nb0 = (g + h.has_leaf + DPB - 1) / DPB;  // blocks of phase A
   const std::uint32_t A = h.n_alias_groups, NG = h.n_groups, A1 = h.n_single_alias;
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
   mulhilo(kPhiloxM0, traj, thi0, tlo0);
 
+  // Predicate (engine.hpp:328-332): lane r checks terms r, r+LPT, ...; the
+  // sub-warp vote combines them. Called by every lane of the sub-warp.
   auto pred_eval = [&](const std::uint32_t* S) -> std::uint32_t {
-    std::uint32_t ok = rp.pred.n ? 1u : 0u;
-#pragma unroll
-    for (std::uint32_t i = 0; i < 4; ++i)
-      if (i < rp.pred.n) ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
-    for (std::uint32_t i = 4; i < rp.pred.n; ++i)
-      ok &= (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i] ? 1u : 0u;
-    return ok;
+    bool ok = true;
+    if constexpr (LPT >= kMaxPredWords) {
+      if (r < rp.pred.n) ok = (S[rp.pred.w[r]] & rp.pred.mask[r]) == rp.pred.want[r];
+    } else {
+      for (std::uint32_t i = r; i < rp.pred.n; i += LPT)
+        ok = ok && (S[rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i];
+    }
+    return rp.pred.n != 0 && __all_sync(smask, ok) ? 1u : 0u;
   };
 
   // Combined-function choice of alias group (engine.hpp:284-291) from draw jj
-  // of the draw buffer.
-  auto alias_pick = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
+  // of the draw buffer, fast form: U53 integer cells (dev_plan.h a53) — `rare`
+  // is set for draws on a cell boundary (about N in 2^32) and for launches or
+  // groups that take the FP64 path, whose choice alias_exact then recomputes;
+  // U32 integer cells (exact, never rare). Branch-free, so the two groups of a
+  // round pair keep independent dependency chains.
+  auto alias_fast = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj,
+                        bool& rare) -> std::uint32_t {
     if constexpr (STREAM == STREAM_U53) {
-      // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
-      // contraction, exactly as engine.hpp:285-290 computes it.
-      const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
-      const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
-      const double xx = __dmul_rn(u, __uint2double_rn(asz));
-      std::uint32_t c = __double2uint_rz(xx);
-      if (c >= asz) c = asz - 1;
-      const double fr = __dsub_rn(xx, __uint2double_rn(c));
-      return fr < ldp<GC>(acut + ab + c) ? c : ldp<GC>(aidx + ab + c);
+      const std::uint32_t hi = dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
+      const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
+      const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
+      const uint2 V = ldp<GC>(a53 + ab + e);  // {alias, hi32 of the cut point}
+      rare = rare || static_cast<std::uint32_t>(P) > ~asz || hi == V.y;
+      return hi < V.y ? e : V.x;
     } else {
       // x*N < 2^53 is exact, so floor and fraction are the product's halves
       const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
@@ -277,6 +294,25 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       const uint2 cell = ldp<GC>(a32 + ab + c);
       return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
     }
+  };
+  // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
+  // contraction, exactly as engine.hpp:285-290 computes it (U53 only).
+  auto alias_exact = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
+    const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+    const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
+    const double xx = __dmul_rn(u, __uint2double_rn(asz));
+    std::uint32_t c = __double2uint_rz(xx);
+    if (c >= asz) c = asz - 1;
+    const double fr = __dsub_rn(xx, __uint2double_rn(c));
+    return fr < __ldg(acut + ab + c) ? c : __ldg(aidx + ab + c);
+  };
+  auto alias_pick = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj,
+                        bool exact) -> std::uint32_t {
+    bool rare = exact;
+    std::uint32_t c = alias_fast(asz, ab, jj, rare);
+    if constexpr (STREAM == STREAM_U53)
+      if (__builtin_expect(rare, 0)) c = alias_exact(asz, ab, jj);
+    return c;
   };
 
   // Gathered parent valuation of combined function record F (engine.hpp:292-302).
@@ -303,7 +339,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     const std::uint32_t asz = G.w & 0x7FFFFFu;
     members = (G.w >> 24) + 1;
     off = G.x;
-    const std::uint32_t idx = asz != 0 ? alias_pick(asz, G.z, jj) : 0u;
+    const std::uint32_t idx =
+        asz != 0 ? alias_pick(asz, G.z, jj, exact_all || (G.w & kGroupExactAlias)) : 0u;
     const uint4 F = ldp<GC>(fns + G.y + idx);
     const std::uint32_t v = gather_fn(Sc, F);
     ohi = 0;
@@ -359,13 +396,22 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   };
   const std::uint32_t zrec01 = zrec(4) | (zrec(5) << 16), zrec23 = zrec(6) | (zrec(7) << 16);
 
-  // Output bit of single-node alias group j (offset j, inline 1-bit table):
-  // loads and shuffles only, so two calls can be interleaved by the scheduler.
-  auto single_bit = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t j,
-                        std::uint32_t jj) -> std::uint32_t {
+  // Single-node alias group j (offset j, inline 1-bit table): the chosen
+  // function's index (rare: see alias_fast), then its output bit — loads and
+  // shuffles only, so two groups can be interleaved by the scheduler.
+  auto single_fn = [&](std::uint32_t j, std::uint32_t jj, bool& rare) -> std::uint32_t {
     const std::uint32_t ar = ldp<GC>(arec + j);
     const std::uint32_t base = ar & 0xFFFFFFu;
-    const uint4 F = ldp<GC>(fns + base + alias_pick(ar >> 24, base, jj));
+    rare = exact_all;
+    return base + alias_fast(ar >> 24, base, jj, rare);
+  };
+  auto single_fn_exact = [&](std::uint32_t j, std::uint32_t jj) -> std::uint32_t {
+    const std::uint32_t ar = ldp<GC>(arec + j);
+    const std::uint32_t base = ar & 0xFFFFFFu;
+    return base + alias_exact(ar >> 24, base, jj);
+  };
+  auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> std::uint32_t {
+    const uint4 F = ldp<GC>(fns + f);
     std::uint32_t v;
     if constexpr (RG) {
       v = gather4_shfl(wreg, F.z, F.w, 0);
@@ -378,6 +424,14 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       v = gather_fn(Sc, F);
     }
     return (F.x >> v) & 1u;
+  };
+  auto single_bit = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t j,
+                        std::uint32_t jj) -> std::uint32_t {
+    bool rare;
+    std::uint32_t f = single_fn(j, jj, rare);
+    if constexpr (STREAM == STREAM_U53)
+      if (__builtin_expect(rare, 0)) f = single_fn_exact(j, jj);
+    return single_out(Sc, wreg, f);
   };
   // A single-node round's ballot word lands at bit jr of the next state.
   // full: all LPT groups of the round exist (a partial last round shares its
@@ -404,7 +458,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     prev = tp & 3u;
     kphase = tp >> 2;
   }
-  std::uint32_t n00 = 0, n01 = 0, n10 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
+  // sampled transitions as four sums over samples with a previous sample:
+  // nv samples, np1 with prev = 1, nh1 with hit = 1, n11 with both
+  // (n10 = np1 - n11, n01 = nh1 - n11, n00 = nv - np1 - nh1 + n11)
+  std::uint32_t nv = 0, np1 = 0, nh1 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
   std::uint32_t* ser = rp.series ? rp.series + tloc * rp.series_stride : nullptr;
   std::uint32_t sword = 0;   // series bits of the current word (lane r == 0)
   if (ser && r == 0 && rp.series_init && rp.series_bit0 > 0 && z0) {
@@ -422,16 +479,17 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     // before the last group, the k'-bit mask for the last group (engine.hpp:
     // 261) and nothing for the leaf draw and the block's unused tail.
     bool flip = false, leaf = false;
-    const bool bern = h.pert_mode != 0;  // Method_old / Method_reduction plans
-    for (std::uint32_t b = r; b < nb0; b += LPT) {
+    // one Philox block of phase A: draws b*DPB .. b*DPB+DPB-1
+    auto phase_a_block = [&](std::uint32_t b, auto bern_c) {
+      constexpr bool BERN = decltype(bern_c)::value;  // Method_old / Method_reduction plans
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
       const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e) {
         std::uint32_t c;
-        if (bern) {  // per-node flip iff u < p (engine.hpp:198)
+        if constexpr (BERN) {  // per-node flip iff u < p (engine.hpp:198)
           if constexpr (STREAM == STREAM_U53)
-            c = pick53(x, e).value() < h.pthr53 ? 1u : 0u;
+            c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
           else
             c = pick32(x, e) < h.pthr32 ? 1u : 0u;
         } else if constexpr (STREAM == STREAM_U53) {
@@ -449,12 +507,23 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         }
         if (q == -1 && h.has_leaf) {  // this element is the leaf draw (engine.hpp:268)
           if constexpr (STREAM == STREAM_U53)
-            leaf = pick53(x, e).value() > h.leaf_thr53;
+            leaf = pick53(x, e).raw() > h.leaf_thr53;
           else
             leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
         }
       }
-    }
+    };
+    auto phase_a = [&](auto bern_c) {
+      if (nb0 <= LPT) {  // launch-uniform: at most one block per lane
+        if (r < nb0) phase_a_block(r, bern_c);
+      } else {
+        for (std::uint32_t b = r; b < nb0; b += LPT) phase_a_block(b, bern_c);
+      }
+    };
+    if (h.pert_mode != 0)  // plan-uniform
+      phase_a(std::true_type{});
+    else
+      phase_a(std::false_type{});
     const bool any_flip = __ballot_sync(smask, flip) != 0;
     const bool any_leaf = __ballot_sync(smask, leaf) != 0;
 
@@ -469,21 +538,47 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
       // alias region: chunks of LPT*DPB draws; lane r first computes phase-B
       // block nb0 + j0/DPB + r into the draw buffer
-      for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB) {
-        if (j0 + r * DPB < A) {
-          const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
-          *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
+      // lane r computes blocks q*LPT + r of each chunk (independent chains)
+      uint4 xb[CB];
+      if constexpr (kPhiloxPipeline) {
+#pragma unroll
+        for (std::uint32_t q = 0; q < CB; ++q)
+          xb[q] = philox_block(sp, nb0 + q * LPT + r, rp.rk0, rp.rk1);
+      }
+      for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB * CB) {
+        if constexpr (!kPhiloxPipeline) {
+#pragma unroll
+          for (std::uint32_t q = 0; q < CB; ++q)
+            xb[q] = philox_block(sp, nb0 + j0 / DPB + q * LPT + r, rp.rk0, rp.rk1);
         }
+#pragma unroll
+        for (std::uint32_t q = 0; q < CB; ++q)
+          if (j0 + (q * LPT + r) * DPB < A)
+            *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
         __syncwarp(smask);
+        if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
+#pragma unroll
+          for (std::uint32_t q = 0; q < CB; ++q)
+            xb[q] = philox_block(sp, nb0 + (j0 / DPB) + (CB + q) * LPT + r, rp.rk0, rp.rk1);
+        }
         // rounds are taken in pairs: both rounds' loads are issued before
         // either ballot/store, so the two dependency chains overlap
 #pragma unroll
-        for (std::uint32_t t = 0; t < DPB; t += 2) {
+        for (std::uint32_t t = 0; t < DPB * CB; t += 2) {
           const std::uint32_t jr0 = j0 + t * LPT, jr1 = jr0 + LPT;
           if (jr0 >= A) break;
           if (jr1 + LPT <= A1) {
-            const std::uint32_t b0 = single_bit(Sc, wreg, jr0 + r, t * LPT + r);
-            const std::uint32_t b1 = single_bit(Sc, wreg, jr1 + r, (t + 1) * LPT + r);
+            bool rare0, rare1;
+            std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
+            std::uint32_t f1 = single_fn(jr1 + r, (t + 1) * LPT + r, rare1);
+            if constexpr (STREAM == STREAM_U53) {
+              if (__builtin_expect(rare0 || rare1, 0)) {
+                if (rare0) f0 = single_fn_exact(jr0 + r, t * LPT + r);
+                if (rare1) f1 = single_fn_exact(jr1 + r, (t + 1) * LPT + r);
+              }
+            }
+            const std::uint32_t b0 = single_out(Sc, wreg, f0);
+            const std::uint32_t b1 = single_out(Sc, wreg, f1);
             store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
             store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
             continue;
@@ -532,10 +627,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     nhit += hit;
     if (++kphase == rp.kappa) {
       kphase = 0;
-      n00 += (prev == 0) & (hit == 0);
-      n01 += (prev == 0) & (hit == 1);
-      n10 += (prev == 1) & (hit == 0);
-      n11 += (prev == 1) & (hit == 1);
+      const std::uint32_t valid = (prev >> 1) ^ 1u;  // prev 2 = none
+      nv += valid;
+      np1 += prev & 1u;
+      nh1 += hit & valid;
+      n11 += prev & hit;
       prev = hit;
     }
     if (rp.node_counts) {  // launch-uniform branch
@@ -574,9 +670,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     const bool pr = rp.pred.n != 0;
     c[0] = rp.n_steps;
     c[1] = pr ? nhit : 0;
-    c[2] = pr ? n00 : 0;
-    c[3] = pr ? n01 : 0;
-    c[4] = pr ? n10 : 0;
+    c[2] = pr ? nv - np1 - nh1 + n11 : 0;
+    c[3] = pr ? nh1 - n11 : 0;
+    c[4] = pr ? np1 - n11 : 0;
     c[5] = pr ? n11 : 0;
     c[6] = nfn;
     c[7] = npert;
@@ -704,7 +800,7 @@ kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, bool rg) {
 }
 
 std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
-  return (2 * h.sw32 + lpt * 4 + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
+  return (2 * h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
 }
 
 cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,

@@ -25,6 +25,66 @@ void put(std::vector<std::uint8_t>& blob, std::size_t off, const std::vector<T>&
 
 }  // namespace
 
+// Exact restatement of the reference's combined-function choice for one
+// draw r53 (engine.hpp:285-290): u = r53 * 2^-53, x = u * N in IEEE double
+// (this file is compiled without FP contraction), c = trunc(x) clamped to
+// N-1, pick c iff x - c < cut[c].
+std::uint32_t alias53_cell(std::uint64_t r53, std::uint32_t n) {
+  const double x = static_cast<double>(r53) * 0x1.0p-53 * static_cast<double>(n);
+  const std::uint32_t c = static_cast<std::uint32_t>(x);
+  return c >= n ? n - 1 : c;
+}
+double alias53_frac(std::uint64_t r53, std::uint32_t n) {
+  const double x = static_cast<double>(r53) * 0x1.0p-53 * static_cast<double>(n);
+  const std::uint32_t c = alias53_cell(r53, n);
+  return x - static_cast<double>(c);
+}
+
+// For each cell c, the smallest r53 of the cell whose fraction reaches cut[c]
+// (the cell's end when none does): within a cell the fraction is monotone in
+// r53, so pick(r53) == c  <=>  r53 < C[c]. Binary searches over the exact rule.
+std::vector<std::uint64_t> alias53_cut_points(const double* cut, std::uint32_t n) {
+  auto first = [&](std::uint64_t lo, std::uint64_t hi, auto pred) {  // min r in [lo,hi) with pred, else hi
+    while (lo < hi) {
+      const std::uint64_t mid = lo + (hi - lo) / 2;
+      if (pred(mid))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    return lo;
+  };
+  const std::uint64_t end = 1ull << 53;
+  std::vector<std::uint64_t> start(n + 1, end), C(n, end);
+  start[0] = 0;
+  for (std::uint32_t c = 1; c < n; ++c)
+    start[c] = first(start[c - 1], end, [&](std::uint64_t r) { return alias53_cell(r, n) >= c; });
+  for (std::uint32_t c = 0; c < n; ++c)
+    C[c] = first(start[c], start[c + 1],
+                 [&](std::uint64_t r) { return !(alias53_frac(r, n) < cut[c]); });
+  return C;
+}
+
+std::vector<std::uint32_t> alias53_records(const double* cut, const std::uint32_t* alias,
+                                           std::uint32_t n) {
+  const std::vector<std::uint64_t> C = alias53_cut_points(cut, n);
+  std::vector<std::uint32_t> rec(2 * static_cast<std::size_t>(n));
+  for (std::uint32_t c = 0; c < n; ++c) {
+    rec[2 * c] = alias[c];
+    rec[2 * c + 1] = static_cast<std::uint32_t>(std::min<std::uint64_t>(C[c], (1ull << 53) - 1) >> 21);
+  }
+  return rec;
+}
+
+std::uint32_t alias53_pick_int(const std::uint32_t* rec, std::uint32_t n, std::uint32_t hi,
+                               bool& rare) {
+  const std::uint64_t P = static_cast<std::uint64_t>(hi) * n;
+  const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
+  const std::uint32_t chi = rec[2 * e + 1];
+  rare = rare || static_cast<std::uint32_t>(P) > ~n || hi == chi;
+  return hi < chi ? e : rec[2 * e];
+}
+
 void philox_round_keys(std::uint64_t seed, std::uint32_t rk0[10], std::uint32_t rk1[10]) {
   std::uint32_t k0 = static_cast<std::uint32_t>(seed), k1 = static_cast<std::uint32_t>(seed >> 32);
   for (int r = 0; r < 10; ++r) {
@@ -89,12 +149,12 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     if (!(v.pert_p > 0.0 && v.pert_p < 1.0)) throw model_error("perturbation rate must be in (0,1)");
     if (v.pert_k != 1) throw model_error("Bernoulli perturbation needs k = 1");
     // u < p  <=>  r < ceil(p * 2^bits)  (p * 2^bits is exact)
-    h.pthr53 = static_cast<std::uint64_t>(std::ceil(std::ldexp(v.pert_p, 53)));
+    h.pthr53 = static_cast<std::uint64_t>(std::ceil(std::ldexp(v.pert_p, 53))) << 11;
     h.pthr32 = static_cast<std::uint64_t>(std::ceil(std::ldexp(v.pert_p, 32)));
   }
   // leaf perturbation iff u > t  <=>  r > floor(t * 2^bits) (t*2^bits is exact)
   const double t53 = std::floor(std::ldexp(v.t, 53));
-  h.leaf_thr53 = static_cast<std::uint64_t>(t53);
+  h.leaf_thr53 = t53 >= 9007199254740992.0 ? ~0ull : (static_cast<std::uint64_t>(t53) << 11) | 0x7FFu;
   const double t32 = std::floor(std::ldexp(v.t, 32));
   h.leaf_never = v.t >= 1.0 ? 1u : 0u;
   h.leaf_thr32 = t32 >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<std::uint32_t>(t32);
@@ -114,7 +174,8 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
         tt = static_cast<std::uint64_t>(T);
         aa = al;
       }
-      pert53[c] = tt | (aa << (53 - k));
+      // raw-word form: compared against the draw's 64-bit word pair (r53 << 11 | noise)
+      pert53[c] = (tt << 11) | (aa << (64 - k));
     }
     {
       const double T = std::ceil(std::ldexp(cut, 32 - static_cast<int>(k)));
@@ -261,6 +322,19 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     }
   }
 
+  // U53 integer records {alias, hi32 of the cut point} (dev_plan.h a53)
+  std::vector<std::uint32_t> a53(2 * v.n_alias, 0);
+  for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
+    const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
+    if (asz == 0) continue;
+    if (asz > kA53MaxCells) {
+      groups[4 * gi + 3] |= kGroupExactAlias;  // this group always takes the FP64 path
+      continue;
+    }
+    const std::vector<std::uint32_t> rec = alias53_records(v.alias_cut + ab, v.alias_idx + ab, asz);
+    std::copy(rec.begin(), rec.end(), a53.begin() + 2 * static_cast<std::size_t>(ab));
+  }
+
   // ---- assemble
   std::size_t off = 0;
   auto section = [&](std::size_t bytes) {
@@ -273,8 +347,7 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.off_groups = section(4 * groups.size());
   h.off_fns = section(4 * fns.size());
   h.off_grec = section(2 * grec.size());
-  h.off_acut = section(8 * acut.size());
-  h.off_aidx = section(4 * aidx.size());
+  h.off_a53 = section(4 * a53.size());
   h.off_a32 = section(4 * a32.size());
   h.off_arec = section(4 * arec.size());
   h.core_bytes = static_cast<std::uint32_t>(off);
@@ -282,8 +355,13 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.table_bytes = static_cast<std::uint32_t>(off) - h.off_tables;
   h.off_pert32 = section(4 * pert32.size());
   h.off_pert53 = section(8 * pert53.size());
-  h.blob_bytes = static_cast<std::uint32_t>(off);
+  h.blob_bytes = static_cast<std::uint32_t>(off);  // end of the stageable prefix
+  // FP64 cut-offs for the rare exact path: read through L1/L2, never staged
+  h.off_acut = section(8 * acut.size());
+  h.off_aidx = section(4 * aidx.size());
   if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
+  if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
+  ep.total_bytes = static_cast<std::uint32_t>(off);
   ep.blob.assign(off, 0);
   put(ep.blob, h.off_pert53, pert53);
   put(ep.blob, h.off_pert32, pert32);
@@ -292,6 +370,7 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   put(ep.blob, h.off_grec, grec);
   put(ep.blob, h.off_acut, acut);
   put(ep.blob, h.off_aidx, aidx);
+  put(ep.blob, h.off_a53, a53);
   put(ep.blob, h.off_a32, a32);
   put(ep.blob, h.off_arec, arec);
   put(ep.blob, h.off_tables, tables);

@@ -88,6 +88,32 @@ def test_resume_and_shard_invariance(pb, cuda_ok):
     assert np.array_equal(np.vstack([a, b]), full)
 
 
+@pytest.mark.parametrize("case", ["c2", "c5", "c3"])
+def test_integer_alias_path_vs_fp64_path(pb, orc, cuda_ok, case):
+    """U53 combined-function choices: the integer fast path (dev_plan.h a53)
+    and the forced FP64 path give the oracle's results."""
+    plan, pred = _setup(pb, case)
+    eng = pb.GpuEnsemble(plan)
+    fast = eng.simulate(seed=11, n_traj=64, n_steps=300, pred=pred)
+    exact = eng.simulate(seed=11, n_traj=64, n_steps=300, pred=pred, exact_alias=True)
+    ost, ocnt = orc.simulate(plan.view, 11, 0, 64, 300, pred=pred)
+    for st, cnt in (fast, exact):
+        assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+
+
+def test_groups_beyond_integer_alias_range(pb, orc, cuda_ok):
+    """Groups with more than 2048 combined functions always take the FP64 path."""
+    model, terms = pb.generate_model(8, (12, 16), (1, 1), 0.02, 0.0, 2, False, 0)
+    plan = pb.prepare(model, 1 << 40, 12, 18)
+    assert int(np.max(plan.flat().grp_alias_size)) > 2048
+    pred = plan.compile_predicate(terms)
+    eng = pb.GpuEnsemble(plan)
+    for stream in (0, 1):
+        st, cnt = eng.simulate(seed=4, n_traj=128, n_steps=2000, pred=pred, stream=stream)
+        ost, ocnt = orc.simulate(plan.view, 4, 0, 128, 2000, pred=pred, stream=stream)
+        assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+
+
 def test_tiny_network_and_edge_sizes(pb, orc, cuda_ok):
     plan, pred = _setup(pb, "tiny")
     eng = pb.GpuEnsemble(plan)
