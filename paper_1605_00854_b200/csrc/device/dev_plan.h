@@ -31,19 +31,23 @@
 //                      (word32 << 5) | ((bit32 - slot) & 31): a funnel rotate by the
 //                      low 5 bits lands the parent bit at `slot`. Unused slots hold
 //                      the always-zero bit n' (engine.hpp:149-150).
-//   a53[A]        uint2 U53 combined-function cells, integer form of engine.hpp:
-//                      285-290 for groups of N <= 2048 functions: {alias[c], hi32 of
-//                      C[c]}, C[c] = the first r53 of cell c whose fraction reaches
-//                      cut[c] (alias53_cut_points; capped at 2^53-1). From the draw's
-//                      high word hi: P = hi * N, e = P >> 32. Unless (P mod 2^32) > ~N
-//                      (hi is the last high word of bucket e, where the double
-//                      rounding can cross into cell e+1; N < 2^21 keeps it within one
-//                      step) or hi == hi32(C[e]), the choice is hi < hi32(C[e]) ? e :
-//                      alias[e]; the rare rest (about N+1 draws in 2^32) takes the
-//                      exact FP64 path.
-//   a32[A]        uint2 {ceil(cut * 2^32) or 0, alias or self}: U32 integer path
+//   acell[A]      uint4 group alias cells {U53: alias[c], hi32 of C[c]; U32: threshold,
+//                      alias}. U32: {ceil(cut * 2^32) or 0, alias or self}; a draw x
+//                      with P = x * N picks c = P >> 32 iff (P mod 2^32) < threshold.
+//                      U53: integer form of engine.hpp:285-290 for groups of N <= 2048
+//                      functions, C[c] = the first r53 of cell c whose fraction
+//                      reaches cut[c] (alias53_cut_points; capped at 2^53-1). From the
+//                      draw's high word hi: P = hi * N, e = P >> 32. Unless (P mod
+//                      2^32) > ~N (hi is the last high word of bucket e, where the
+//                      double rounding can cross into cell e+1; N < 2^21 keeps it
+//                      within one step) or hi == hi32(C[e]), the choice is
+//                      hi < hi32(C[e]) ? e : alias[e]; the rare rest (about N+1 draws
+//                      in 2^32) takes the exact FP64 path.
 //   arec[A1]      u32  compact record of the leading single-node alias groups:
 //                      base | alias_size << 24 (their fn_begin == alias_begin == base)
+//   sfn[F1]       uint2 (single_compact) compact records of the single-node groups'
+//                      functions: {rec0 | rec1 << 10 | rec2 << 20, rec3 | table << 16}
+//   arec4[A1]     uint4 (single_compact) {acell byte offset, sfn byte offset, N, ~N}
 //   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
 //   acut[A] f64, aidx[A] u32 (exact section): the group cut-offs and targets
 //                      for the FP64 path (boundary draws, groups with N > 2048)
@@ -66,6 +70,10 @@ inline constexpr std::uint32_t kChunkBlocks = PBN_CHUNK_BLOCKS;
 // 1: the next chunk's Philox blocks are computed while the current chunk's
 // rounds run (software pipelining; ALU work overlaps the rounds' load latency)
 inline constexpr bool kPhiloxPipeline = PBN_PHILOX_PIPELINE != 0;
+#ifndef PBN_COMPACT_SINGLE
+#define PBN_COMPACT_SINGLE 1
+#endif
+inline constexpr bool kUseCompactSingle = PBN_COMPACT_SINGLE != 0;  // GM = 2 when the plan allows
 inline constexpr std::uint32_t kA53MaxCells = 2048;           // alias fits the low 11 bits
 inline constexpr std::uint32_t kGroupExactAlias = 1u << 23;   // groups[].w flag: FP64 path only
 
@@ -81,7 +89,7 @@ struct dev_plan_header {
   std::uint32_t leaf_thr32; // floor(t * 2^32) (saturated)
   std::uint32_t leaf_never; // t == 1: the leaf draw can never fire
   std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
-  std::uint32_t off_acut, off_aidx, off_a53, off_a32, off_arec, off_tables;
+  std::uint32_t off_acut, off_aidx, off_acell, off_arec, off_sfn, off_arec4, off_tables;
   std::uint32_t core_bytes;   // bytes [0, off_tables)
   std::uint32_t table_bytes;  // bytes [off_tables, off_pert32)
   std::uint32_t blob_bytes;   // stageable prefix: core | tables | pert32 | pert53
@@ -91,6 +99,7 @@ struct dev_plan_header {
                                  // every function's table inline (1 bit x <= 32 entries)
   std::uint32_t rg_ok;           // sw32 <= 32: one state word per lane fits a warp (SHFL gather)
   std::uint32_t single_gc5;      // some function of groups [0, A1) has 5 parents
+  std::uint32_t single_compact;  // rg_ok, A1 >= 32, no 5-parent function: sfn/arec4 present
   std::uint32_t pert_mode;       // 0 grouped patterns, 1 per-node Bernoulli(p) (Method_old)
   std::uint32_t has_leaf;        // phase A ends with the leaf draw
   std::uint64_t pthr53;          // Bernoulli: flip iff R < ceil(p * 2^53) << 11 (raw word)

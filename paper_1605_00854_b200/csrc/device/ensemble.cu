@@ -165,7 +165,9 @@ __device__ __forceinline__ std::uint32_t gather4_shfl(std::uint32_t wreg, std::u
 // the 148 SMs in one wave), which leaves 72 registers per thread.
 constexpr int kMaxWarpsLpt32 = 28;
 
-template <int LPT, int STREAM, int PLACE, bool RG>
+// GM: parent gather mode — 0 shared-memory state words, 1 one state word per
+// lane with shuffles (RG), 2 RG with the compact single-node records (SC).
+template <int LPT, int STREAM, int PLACE, int GM>
 __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                         const dev_run_params rp, std::uint64_t* __restrict__ states,
@@ -176,6 +178,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool GT = PLACE < PLACE_TABLES;   // tables read from global
   constexpr bool GP = PLACE < PLACE_ALL;      // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
+  constexpr bool RG = GM >= 1;
+  constexpr bool SC = GM == 2;
 
   const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
   if (staged) stage_plan(smem, gblob, staged, &stage_bar);
@@ -191,9 +195,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // FP64 cut-offs of the exact path: never staged (dev_plan.h)
   const double* acut = reinterpret_cast<const double*>(gblob + h.off_acut);
   const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(gblob + h.off_aidx);
-  const uint2* a53 = reinterpret_cast<const uint2*>(core + h.off_a53);
-  const uint2* a32 = reinterpret_cast<const uint2*>(core + h.off_a32);
+  const uint4* acell = reinterpret_cast<const uint4*>(core + h.off_acell);
   const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
+  const uint4* arec4 = reinterpret_cast<const uint4*>(core + h.off_arec4);
 
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t r = lane % LPT;
@@ -284,14 +288,14 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       const std::uint32_t hi = dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
       const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
-      const uint2 V = ldp<GC>(a53 + ab + e);  // {alias, hi32 of the cut point}
+      const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(acell + ab + e));  // {alias, hi32(C)}
       rare = rare || static_cast<std::uint32_t>(P) > ~asz || hi == V.y;
       return hi < V.y ? e : V.x;
     } else {
       // x*N < 2^53 is exact, so floor and fraction are the product's halves
       const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
       const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
-      const uint2 cell = ldp<GC>(a32 + ab + c);
+      const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(acell + ab + c) + 1);  // {thr, alias}
       return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
     }
   };
@@ -396,37 +400,75 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   };
   const std::uint32_t zrec01 = zrec(4) | (zrec(5) << 16), zrec23 = zrec(6) | (zrec(7) << 16);
 
-  // Single-node alias group j (offset j, inline 1-bit table): the chosen
-  // function's index (rare: see alias_fast), then its output bit — loads and
-  // shuffles only, so two groups can be interleaved by the scheduler.
+  // Single-node alias group j (offset j, inline 1-bit table): a handle of the
+  // chosen function (rare: see alias_fast) — its index, or with the compact
+  // records (SC) the byte offset of its sfn record — then its output bit;
+  // loads and shuffles only, so two groups can be interleaved by the scheduler.
   auto single_fn = [&](std::uint32_t j, std::uint32_t jj, bool& rare) -> std::uint32_t {
-    const std::uint32_t ar = ldp<GC>(arec + j);
-    const std::uint32_t base = ar & 0xFFFFFFu;
     rare = exact_all;
-    return base + alias_fast(ar >> 24, base, jj, rare);
+    if constexpr (SC) {
+      const uint4 ar = ldp<GC>(arec4 + j);  // {acell offset, sfn offset, N, ~N}
+      std::uint32_t pick;
+      if constexpr (STREAM == STREAM_U53) {
+        const std::uint32_t hi = dbuf[2 * jj + 1];
+        const std::uint64_t P = static_cast<std::uint64_t>(hi) * ar.z;
+        const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
+        const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 16 * e));
+        rare = rare || static_cast<std::uint32_t>(P) > ar.w || hi == V.y;
+        pick = hi < V.y ? e : V.x;
+      } else {
+        const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * ar.z;
+        const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
+        const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 16 * c + 8));
+        pick = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
+      }
+      return ar.y + 8 * pick;
+    } else {
+      const std::uint32_t ar = ldp<GC>(arec + j);
+      const std::uint32_t base = ar & 0xFFFFFFu;
+      return base + alias_fast(ar >> 24, base, jj, rare);
+    }
   };
   auto single_fn_exact = [&](std::uint32_t j, std::uint32_t jj) -> std::uint32_t {
     const std::uint32_t ar = ldp<GC>(arec + j);
     const std::uint32_t base = ar & 0xFFFFFFu;
-    return base + alias_exact(ar >> 24, base, jj);
+    const std::uint32_t f = base + alias_exact(ar >> 24, base, jj);
+    if constexpr (SC)
+      return h.off_sfn + 8 * f;
+    else
+      return f;
   };
-  auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> std::uint32_t {
-    const uint4 F = ldp<GC>(fns + f);
-    std::uint32_t v;
-    if constexpr (RG) {
-      v = gather4_shfl(wreg, F.z, F.w, 0);
-      if (h.single_gc5) {  // plan-uniform: every lane takes the same branch
-        uint2 rr = make_uint2(zrec01, zrec23);
-        if ((F.y & 31u) > 4) rr = ldp<GC>(grec + (F.y >> 8));
-        v |= gather4_shfl(wreg, rr.x, rr.y, 4);
-      }
+  auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
+    if constexpr (SC) {
+      // compact record: 10-bit records (word << 5 | rotation), table at bits 16..31
+      const uint2 F = ldp<GC>(reinterpret_cast<const uint2*>(core + f));
+      const std::uint32_t w0 = __shfl_sync(0xFFFFFFFFu, wreg, F.x >> 5);
+      const std::uint32_t w1 = __shfl_sync(0xFFFFFFFFu, wreg, F.x >> 15);
+      const std::uint32_t w2 = __shfl_sync(0xFFFFFFFFu, wreg, F.x >> 25);
+      const std::uint32_t w3 = __shfl_sync(0xFFFFFFFFu, wreg, F.y >> 5);
+      const std::uint32_t v = 16u | (__funnelshift_r(w0, w0, F.x) & 1u) |
+                              (__funnelshift_r(w1, w1, F.x >> 10) & 2u) |
+                              (__funnelshift_r(w2, w2, F.x >> 20) & 4u) |
+                              (__funnelshift_r(w3, w3, F.y) & 8u);
+      return (F.y >> v) & 1u;
     } else {
-      v = gather_fn(Sc, F);
+      const uint4 F = ldp<GC>(fns + f);
+      std::uint32_t v;
+      if constexpr (RG) {
+        v = gather4_shfl(wreg, F.z, F.w, 0);
+        if (h.single_gc5) {  // plan-uniform: every lane takes the same branch
+          uint2 rr = make_uint2(zrec01, zrec23);
+          if ((F.y & 31u) > 4) rr = ldp<GC>(grec + (F.y >> 8));
+          v |= gather4_shfl(wreg, rr.x, rr.y, 4);
+        }
+      } else {
+        v = gather_fn(Sc, F);
+      }
+      return (F.x >> v) & 1u;
     }
-    return (F.x >> v) & 1u;
   };
   auto single_bit = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t j,
-                        std::uint32_t jj) -> std::uint32_t {
+                        std::uint32_t jj) -> bool {
     bool rare;
     std::uint32_t f = single_fn(j, jj, rare);
     if constexpr (STREAM == STREAM_U53)
@@ -438,14 +480,12 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // word with the next region and must OR atomically).
   auto store_bits = [&](std::uint32_t* Sn, std::uint32_t jr, std::uint32_t bits, bool full) {
     if constexpr (LPT < 32) bits = (bits >> (sub * LPT)) & ((1u << (LPT & 31)) - 1u);
-    if (r == 0 && bits) {
+    if (LPT == 32 && full) {
+      if (r == 0) Sn[jr >> 5] = bits;  // jr is a multiple of 32: the word is this round's alone
+    } else if (r == 0 && bits) {
       const std::uint32_t w = jr >> 5, sh = jr & 31;
-      if (LPT == 32 && full) {
-        Sn[w] = bits;  // jr is a multiple of 32: the word is this round's alone
-      } else {
-        atomicOr(Sn + w, bits << sh);
-        if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
-      }
+      atomicOr(Sn + w, bits << sh);
+      if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
     }
   };
 
@@ -577,8 +617,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                 if (rare1) f1 = single_fn_exact(jr1 + r, (t + 1) * LPT + r);
               }
             }
-            const std::uint32_t b0 = single_out(Sc, wreg, f0);
-            const std::uint32_t b1 = single_out(Sc, wreg, f1);
+            const bool b0 = single_out(Sc, wreg, f0);
+            const bool b1 = single_out(Sc, wreg, f1);
             store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
             store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
             continue;
@@ -594,8 +634,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             } else if (A1 == A) {
               // partial last round of an all-single-node alias region: lanes
               // past the region evaluate a valid group and drop the bit
-              const std::uint32_t b = single_bit(Sc, wreg, j < A ? j : A - 1, (t + u) * LPT + r);
-              store_bits(Sn, jr, __ballot_sync(smask, j < A ? b : 0u), false);
+              const bool b = single_bit(Sc, wreg, j < A ? j : A - 1, (t + u) * LPT + r);
+              store_bits(Sn, jr, __ballot_sync(smask, j < A && b), false);
             } else {
               const bool act = j < A;
               std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
@@ -762,41 +802,43 @@ __global__ void pbn_philox_kat_kernel(const uint4* ctr, std::uint32_t k0, std::u
 using kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
                            std::uint64_t*, std::uint64_t*);
 
-template <int LPT, int STREAM, bool RG>
+template <int LPT, int STREAM, int GM>
 kernel_fn pick_place(int place) {
   switch (place) {
     case PLACE_ALL:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, RG>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, GM>;
     case PLACE_TABLES:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, RG>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, GM>;
     case PLACE_CORE:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, RG>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, GM>;
     default:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL, RG>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL, GM>;
   }
 }
 
 template <int STREAM>
-kernel_fn pick_lpt(std::uint32_t lpt, int place, bool rg) {
+kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
   switch (lpt) {
     case 1:
-      return pick_place<1, STREAM, false>(place);
+      return pick_place<1, STREAM, 0>(place);
     case 2:
-      return pick_place<2, STREAM, false>(place);
+      return pick_place<2, STREAM, 0>(place);
     case 4:
-      return pick_place<4, STREAM, false>(place);
+      return pick_place<4, STREAM, 0>(place);
     case 8:
-      return pick_place<8, STREAM, false>(place);
+      return pick_place<8, STREAM, 0>(place);
     case 16:
-      return pick_place<16, STREAM, false>(place);
+      return pick_place<16, STREAM, 0>(place);
     default:
-      return rg ? pick_place<32, STREAM, true>(place) : pick_place<32, STREAM, false>(place);
+      return gm == 2   ? pick_place<32, STREAM, 2>(place)
+             : gm == 1 ? pick_place<32, STREAM, 1>(place)
+                       : pick_place<32, STREAM, 0>(place);
   }
 }
 
-kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, bool rg) {
-  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, rg)
-                              : pick_lpt<STREAM_U32>(lpt, place, rg);
+kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm) {
+  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, gm)
+                              : pick_lpt<STREAM_U32>(lpt, place, gm);
 }
 
 std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
@@ -809,7 +851,8 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches) {
   const bool rg = lpt == 32 && h.rg_ok && h.n_single_alias >= 32;
-  const kernel_fn fn = select_kernel(lpt, stream_kind, place, rg);
+  const int gm = !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
+  const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm);
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;

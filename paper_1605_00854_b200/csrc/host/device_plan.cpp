@@ -305,7 +305,8 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   // ---- group alias cells
   std::vector<double> acut(v.alias_cut, v.alias_cut + v.n_alias);
   std::vector<std::uint32_t> aidx(v.alias_idx, v.alias_idx + v.n_alias);
-  std::vector<std::uint32_t> a32(2 * v.n_alias);
+  // acell[c] = {U53: alias, hi32 of the cut point (dev_plan.h); U32: threshold, alias}
+  std::vector<std::uint32_t> acell(4 * v.n_alias, 0);
   h.u32_ok = h.max_alias <= (1u << 21) ? 1u : 0u;
   for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
     const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
@@ -317,22 +318,43 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
         tt = static_cast<std::uint32_t>(T);
         aa = v.alias_idx[ab + c];
       }
-      a32[2 * (ab + c) + 0] = tt;
-      a32[2 * (ab + c) + 1] = aa;
+      acell[4 * (ab + c) + 2] = tt;
+      acell[4 * (ab + c) + 3] = aa;
     }
-  }
-
-  // U53 integer records {alias, hi32 of the cut point} (dev_plan.h a53)
-  std::vector<std::uint32_t> a53(2 * v.n_alias, 0);
-  for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
-    const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
     if (asz == 0) continue;
     if (asz > kA53MaxCells) {
       groups[4 * gi + 3] |= kGroupExactAlias;  // this group always takes the FP64 path
       continue;
     }
     const std::vector<std::uint32_t> rec = alias53_records(v.alias_cut + ab, v.alias_idx + ab, asz);
-    std::copy(rec.begin(), rec.end(), a53.begin() + 2 * static_cast<std::size_t>(ab));
+    for (std::uint32_t c = 0; c < asz; ++c) {
+      acell[4 * (ab + c) + 0] = rec[2 * c];
+      acell[4 * (ab + c) + 1] = rec[2 * c + 1];
+    }
+  }
+
+  // compact records of the leading single-node groups for the register gather
+  // (n' <= 1023, at most 4 parents): sfn[f] = {rec0 | rec1 << 10 | rec2 << 20,
+  // rec3 | table << 16} with 10-bit records (word << 5 | rotation), and
+  // arec4[j] = {byte offset of the group's acell, byte offset of its sfn, N, ~N}
+  h.single_compact = h.rg_ok && h.n_single_alias >= 32 && !h.single_gc5 ? 1u : 0u;
+  std::vector<std::uint32_t> sfn, arec4;
+  std::uint32_t n_sfn = 0;
+  if (h.single_compact) {
+    for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi)
+      n_sfn = std::max(n_sfn, v.grp_fn_begin[gi] + v.grp_alias_size[gi]);
+    sfn.assign(2 * static_cast<std::size_t>(n_sfn), 0);
+    for (std::uint32_t f = 0; f < n_sfn; ++f) {
+      const std::uint32_t gc = v.fn_gather_count[f];
+      if (gc > 4 || fn_members[f] != 1) throw model_error("compact single-node record misuse");
+      std::uint32_t rc[4];
+      for (std::uint32_t b = 0; b < 4; ++b) rc[b] = record(f, b) & 0x3FFu;
+      std::uint32_t table = 0;
+      for (std::uint32_t e = 0; e < (1u << gc); ++e)
+        table |= static_cast<std::uint32_t>(v.fn_tables[v.fn_table_begin[f] + e] & 1u) << e;
+      sfn[2 * f] = rc[0] | (rc[1] << 10) | (rc[2] << 20);
+      sfn[2 * f + 1] = rc[3] | (table << 16);
+    }
   }
 
   // ---- assemble
@@ -347,9 +369,10 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.off_groups = section(4 * groups.size());
   h.off_fns = section(4 * fns.size());
   h.off_grec = section(2 * grec.size());
-  h.off_a53 = section(4 * a53.size());
-  h.off_a32 = section(4 * a32.size());
+  h.off_acell = section(4 * acell.size());
   h.off_arec = section(4 * arec.size());
+  h.off_sfn = section(4 * sfn.size());
+  h.off_arec4 = section(16 * static_cast<std::size_t>(h.single_compact ? h.n_single_alias : 0));
   h.core_bytes = static_cast<std::uint32_t>(off);
   h.off_tables = section(tables.size());
   h.table_bytes = static_cast<std::uint32_t>(off) - h.off_tables;
@@ -370,9 +393,20 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   put(ep.blob, h.off_grec, grec);
   put(ep.blob, h.off_acut, acut);
   put(ep.blob, h.off_aidx, aidx);
-  put(ep.blob, h.off_a53, a53);
-  put(ep.blob, h.off_a32, a32);
+  put(ep.blob, h.off_acell, acell);
   put(ep.blob, h.off_arec, arec);
+  put(ep.blob, h.off_sfn, sfn);
+  if (h.single_compact) {
+    arec4.assign(4 * static_cast<std::size_t>(h.n_single_alias), 0);
+    for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi) {
+      const std::uint32_t asz = v.grp_alias_size[gi], base = v.grp_fn_begin[gi];
+      arec4[4 * gi + 0] = h.off_acell + 16 * v.grp_alias_begin[gi];
+      arec4[4 * gi + 1] = h.off_sfn + 8 * base;
+      arec4[4 * gi + 2] = asz;
+      arec4[4 * gi + 3] = ~asz;
+    }
+    put(ep.blob, h.off_arec4, arec4);
+  }
   put(ep.blob, h.off_tables, tables);
   return ep;
 }
