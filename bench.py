@@ -523,8 +523,8 @@ def run_ours(a):
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                      "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-                     "issue_bound_evidence": "profiles/r01_c2_final_u53.txt: issue slots ~72% "
-                                             "busy, ALU pipe ~69%, smem wavefronts ~62%",
+                     "issue_bound_evidence": "profiles/r01_c2_k16_u53_v4.txt: issue slots ~71% "
+                                             "busy, ALU pipe ~67%, smem wavefronts ~68%",
                      "note": "lookup roofline = SMs x 32 probes/clk x sm_max_mhz "
                              "(MEASURED_PEAKS.json); algorithmic lookups = g per step + "
                              "(A+G) per function-phase step (SURVEY 8d), per GPU",
