@@ -303,6 +303,9 @@ def run_estimate_mode(a, torch, dist, rank, world, local, dev):
     e2e = None
     if world == 1:
         h_states = np.zeros((n_total, eng.words), np.uint64)
+        pb.estimate(eng, pred, pb.make_request(  # untimed warm-up of the C-ABI path
+            precision=1e-3, confidence=0.95, pilot=pilot, seed=999, n_traj=n_total,
+            stream=stream), h_states.copy())
         t0 = time.perf_counter()
         e_steps = 0
         for k in range(a.steps):

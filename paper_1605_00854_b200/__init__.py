@@ -239,7 +239,7 @@ class Model:
         self._h = C.c_void_p(handle)
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if lib is not None and getattr(self, "_h", None) and self._h.value:
             lib.pbn_model_free(self._h)
             self._h = C.c_void_p(None)
 
@@ -354,7 +354,7 @@ class PreparedSimulation:
         _check(lib.pbn_plan_get_view(self._h, C.byref(self._view)))
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if lib is not None and getattr(self, "_h", None) and self._h.value:
             lib.pbn_plan_free(self._h)
             self._h = C.c_void_p(None)
 
@@ -491,7 +491,7 @@ class GpuEnsemble:
             self.set_placement(placement)
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if lib is not None and getattr(self, "_h", None) and self._h.value:
             lib.pbn_gpu_destroy(self._h)
             self._h = C.c_void_p(None)
 

@@ -649,10 +649,13 @@ struct dev_buf {
   }
   dev_buf(const dev_buf&) = delete;
   dev_buf& operator=(const dev_buf&) = delete;
+  void swap(dev_buf& o) { std::swap(p, o.p); }
 };
 
 // Device ensemble: states, carried thin samples, pilot series and count
-// records stay in HBM; each round returns 8 pooled counters.
+// records stay in HBM; each round returns 8 pooled counters. The pilot series
+// buffer starts at the requested pilot length and grows (row copy) only when
+// the estimator widens the pilot; its capacity bound is 2^33 bits in total.
 class device_backend : public estimator_backend {
  public:
   device_backend(pbn_gpu& g, const pbn_estimate_request& req, const std::uint32_t* bits,
@@ -661,7 +664,8 @@ class device_backend : public estimator_backend {
         words_(pbn_state_words(g.ep.h.n_kept)),
         cap_(std::min<std::uint64_t>(1ull << 22,
                                      std::max<std::uint64_t>(1024, (1ull << 33) / std::max(1u, req.n_traj)))),
-        stride_((cap_ + 31) / 32),
+        stride_(std::min<std::uint64_t>((cap_ + 31) / 32,
+                                        (std::max<std::uint64_t>(req.pilot, 100) + 32) / 32)),
         states_(static_cast<std::size_t>(req.n_traj) * words_),
         counts_(static_cast<std::size_t>(req.n_traj) * PBN_COUNT_FIELDS),
         tprev_(req.n_traj),
@@ -677,10 +681,25 @@ class device_backend : public estimator_backend {
   void download(std::uint64_t* host) {
     ck(cudaMemcpy(host, states_.p, 8 * words_ * req_.n_traj, cudaMemcpyDeviceToHost), "D2H");
   }
+  // make every row hold series positions [0, bits)
+  void reserve_series(std::uint64_t bits) {
+    const std::uint64_t need = (bits + 31) / 32;
+    if (need <= stride_) return;
+    const std::uint64_t stride = std::min<std::uint64_t>((cap_ + 31) / 32, std::max(need, 2 * stride_));
+    dev_buf<std::uint32_t> grown(static_cast<std::size_t>(req_.n_traj) * stride);
+    ck(cudaMemset(grown.p, 0, sizeof(std::uint32_t) * req_.n_traj * stride), "memset");
+    ck(cudaMemcpy2D(grown.p, 4 * stride, series_.p, 4 * stride_, 4 * stride_, req_.n_traj,
+                    cudaMemcpyDeviceToDevice),
+       "series grow");
+    series_.swap(grown);
+    stride_ = stride;
+  }
   void run(std::uint64_t step_begin, std::uint64_t n_steps, std::uint32_t kappa,
            std::uint32_t thin_mode, std::uint64_t series_bit0, bool series_init,
            std::uint64_t totals[PBN_COUNT_FIELDS]) override {
     for (int i = 0; i < PBN_COUNT_FIELDS; ++i) totals[i] = 0;
+    if (series_bit0 != std::numeric_limits<std::uint64_t>::max())
+      reserve_series(series_bit0 + n_steps);
     std::uint64_t done = 0;
     while (done < n_steps) {  // at most 2^31 steps per launch
       const std::uint64_t n = std::min<std::uint64_t>(n_steps - done, 1ull << 31);
