@@ -105,7 +105,7 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // Lanes per trajectory: by network size, then doubled until the ensemble
 // gives ~24 resident warps per SM (latency hiding) or one warp per trajectory.
 std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t sms) {
-  std::uint32_t lpt = n_kept <= 96 ? 4 : n_kept <= 256 ? 8 : n_kept <= 512 ? 16 : 32;
+  std::uint32_t lpt = n_kept <= 256 ? 8 : n_kept <= 512 ? 16 : 32;
   while (lpt < 32 && n_traj * lpt / 32 < static_cast<std::uint64_t>(sms) * 24) lpt *= 2;
   return lpt;
 }

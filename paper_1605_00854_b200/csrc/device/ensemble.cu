@@ -623,6 +623,18 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
             continue;
           }
+          // two general rounds: both groups' loads before either emit (not in
+          // the compact-record variant, whose register budget it would raise)
+          if (!SC && jr0 >= A1) {
+            const std::uint32_t j0 = jr0 + r, j1 = jr1 + r;
+            const bool a0 = j0 < A, a1 = j1 < A;
+            std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
+            if (a0) eval_group(Sc, j0, t * LPT + r, lo0, hi0, off0, m0);
+            if (a1) eval_group(Sc, j1, (t + 1) * LPT + r, lo1, hi1, off1, m1);
+            emit_round(Sn, a0, lo0, hi0, off0, m0);
+            if (jr1 < A) emit_round(Sn, a1, lo1, hi1, off1, m1);
+            continue;
+          }
 #pragma unroll
           for (std::uint32_t u = 0; u < 2; ++u) {
             const std::uint32_t jr = jr0 + u * LPT;
