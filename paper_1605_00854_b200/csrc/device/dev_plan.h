@@ -45,12 +45,21 @@
 //                      in 2^32) takes the exact FP64 path.
 //   arec[A1]      u32  compact record of the leading single-node alias groups:
 //                      base | alias_size << 24 (their fn_begin == alias_begin == base)
-//   sfn[F1]       uint2 (single_compact) compact records of the single-node groups'
-//                      functions: {rec0 | rec1 << 10 | rec2 << 20, rec3 | table << 16}
-//   arec4[A1]     uint4 (single_compact) {acell byte offset, sfn byte offset, N, ~N}
+//   scol          (single_compact) bank-column records of the single-node groups:
+//                      rows of kScolSlots 8-byte slots (128 bytes); group j owns slot
+//                      j % kScolSlots, so a half-warp's 16 lanes of one round read 16
+//                      distinct bank pairs. Per group, consecutive rows of its slot
+//                      hold N U53 cells {alias, hi32(C)}, N U32 cells {threshold,
+//                      alias} and N function records {rec0 | rec1 << 10 | rec2 << 20,
+//                      rec3 | table << 16} (10-bit gather records word << 5 | rotation)
+//   arec4[A1]     uint4 (single_compact) {byte offset of the group's first U53 cell,
+//                      of its first function record, N, ~N}; row stride 128 bytes
 //   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
 //   acut[A] f64, aidx[A] u32 (exact section): the group cut-offs and targets
 //                      for the FP64 path (boundary draws, groups with N > 2048)
+//   fns_s, acell_s     (single_compact) the single-node groups' fns and acell
+//                      entries, moved out of the staged core: the compact kernels
+//                      read scol instead; fallback kernels (other LPT) read these
 #pragma once
 
 #include <cstdint>
@@ -74,7 +83,8 @@ inline constexpr bool kPhiloxPipeline = PBN_PHILOX_PIPELINE != 0;
 #define PBN_COMPACT_SINGLE 1
 #endif
 inline constexpr bool kUseCompactSingle = PBN_COMPACT_SINGLE != 0;  // GM = 2 when the plan allows
-inline constexpr std::uint32_t kA53MaxCells = 2048;           // alias fits the low 11 bits
+inline constexpr std::uint32_t kA53MaxCells = 2048;
+inline constexpr std::uint32_t kScolSlots = 16;          // 8-byte slots per 128-byte row           // alias fits the low 11 bits
 inline constexpr std::uint32_t kGroupExactAlias = 1u << 23;   // groups[].w flag: FP64 path only
 
 struct dev_plan_header {
@@ -89,7 +99,11 @@ struct dev_plan_header {
   std::uint32_t leaf_thr32; // floor(t * 2^32) (saturated)
   std::uint32_t leaf_never; // t == 1: the leaf draw can never fire
   std::uint32_t off_pert53, off_pert32, off_groups, off_fns, off_grec;
-  std::uint32_t off_acut, off_aidx, off_acell, off_arec, off_sfn, off_arec4, off_tables;
+  std::uint32_t off_acut, off_aidx, off_acell, off_arec, off_scol, off_arec4, off_tables;
+  std::uint32_t off_fns_s, off_acell_s;  // single-node groups' fns / acell entries (absolute
+                                         // indices): the unstaged tail when fn_base or
+                                         // cell_base != 0, else = off_fns / off_acell
+  std::uint32_t fn_base, cell_base;      // groups[].y / .z are relative to these
   std::uint32_t core_bytes;   // bytes [0, off_tables)
   std::uint32_t table_bytes;  // bytes [off_tables, off_pert32)
   std::uint32_t blob_bytes;   // stageable prefix: core | tables | pert32 | pert53

@@ -196,6 +196,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const double* acut = reinterpret_cast<const double*>(gblob + h.off_acut);
   const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(gblob + h.off_aidx);
   const uint4* acell = reinterpret_cast<const uint4*>(core + h.off_acell);
+  // single-node groups' fns / acell entries for the non-compact single path
+  // (generic loads: staged or the unstaged tail, dev_plan.h)
+  const std::uint8_t* sbase = (h.fn_base || h.cell_base) ? gblob : core;
+  const uint4* fns_s = reinterpret_cast<const uint4*>(sbase + h.off_fns_s);
+  const uint4* acell_s = reinterpret_cast<const uint4*>(sbase + h.off_acell_s);
   const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
   const uint4* arec4 = reinterpret_cast<const uint4*>(core + h.off_arec4);
 
@@ -282,20 +287,20 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // groups that take the FP64 path, whose choice alias_exact then recomputes;
   // U32 integer cells (exact, never rare). Branch-free, so the two groups of a
   // round pair keep independent dependency chains.
-  auto alias_fast = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj,
-                        bool& rare) -> std::uint32_t {
+  auto alias_fast = [&](const uint4* cells, std::uint32_t asz, std::uint32_t ab,
+                        std::uint32_t jj, bool& rare) -> std::uint32_t {
     if constexpr (STREAM == STREAM_U53) {
       const std::uint32_t hi = dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
       const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
-      const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(acell + ab + e));  // {alias, hi32(C)}
+      const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + e));  // {alias, hi32(C)}
       rare = rare || static_cast<std::uint32_t>(P) > ~asz || hi == V.y;
       return hi < V.y ? e : V.x;
     } else {
       // x*N < 2^53 is exact, so floor and fraction are the product's halves
       const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * asz;
       const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
-      const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(acell + ab + c) + 1);  // {thr, alias}
+      const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + c) + 1);  // {thr, alias}
       return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
     }
   };
@@ -313,9 +318,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   auto alias_pick = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj,
                         bool exact) -> std::uint32_t {
     bool rare = exact;
-    std::uint32_t c = alias_fast(asz, ab, jj, rare);
+    std::uint32_t c = alias_fast(acell, asz, ab, jj, rare);  // ab relative to cell_base
     if constexpr (STREAM == STREAM_U53)
-      if (__builtin_expect(rare, 0)) c = alias_exact(asz, ab, jj);
+      if (__builtin_expect(rare, 0)) c = alias_exact(asz, ab + h.cell_base, jj);
     return c;
   };
 
@@ -402,41 +407,44 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
 
   // Single-node alias group j (offset j, inline 1-bit table): a handle of the
   // chosen function (rare: see alias_fast) — its index, or with the compact
-  // records (SC) the byte offset of its sfn record — then its output bit;
+  // records (SC) the byte offset of its scol function record — then its output bit;
   // loads and shuffles only, so two groups can be interleaved by the scheduler.
   auto single_fn = [&](std::uint32_t j, std::uint32_t jj, bool& rare) -> std::uint32_t {
     rare = exact_all;
     if constexpr (SC) {
-      const uint4 ar = ldp<GC>(arec4 + j);  // {acell offset, sfn offset, N, ~N}
+      const uint4 ar = ldp<GC>(arec4 + j);  // {U53 cell offset, function offset, N, ~N}
       std::uint32_t pick;
       if constexpr (STREAM == STREAM_U53) {
         const std::uint32_t hi = dbuf[2 * jj + 1];
         const std::uint64_t P = static_cast<std::uint64_t>(hi) * ar.z;
         const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
-        const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 16 * e));
+        const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 8 * kScolSlots * e));
         rare = rare || static_cast<std::uint32_t>(P) > ar.w || hi == V.y;
         pick = hi < V.y ? e : V.x;
       } else {
         const std::uint64_t P = static_cast<std::uint64_t>(dbuf[jj]) * ar.z;
         const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
-        const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 16 * c + 8));
+        const uint2 cell =
+            ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 8 * kScolSlots * (ar.z + c)));
         pick = static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
       }
-      return ar.y + 8 * pick;
+      return ar.y + 8 * kScolSlots * pick;
     } else {
       const std::uint32_t ar = ldp<GC>(arec + j);
       const std::uint32_t base = ar & 0xFFFFFFu;
-      return base + alias_fast(ar >> 24, base, jj, rare);
+      if (h.cell_base == 0)  // plan-uniform: entries in the staged acell
+        return base + alias_fast(acell, ar >> 24, base, jj, rare);
+      return base + alias_fast(acell_s, ar >> 24, base, jj, rare);
     }
   };
   auto single_fn_exact = [&](std::uint32_t j, std::uint32_t jj) -> std::uint32_t {
     const std::uint32_t ar = ldp<GC>(arec + j);
     const std::uint32_t base = ar & 0xFFFFFFu;
-    const std::uint32_t f = base + alias_exact(ar >> 24, base, jj);
+    const std::uint32_t pick = alias_exact(ar >> 24, base, jj);
     if constexpr (SC)
-      return h.off_sfn + 8 * f;
+      return ldp<GC>(arec4 + j).y + 8 * kScolSlots * pick;
     else
-      return f;
+      return base + pick;
   };
   auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
     if constexpr (SC) {
@@ -452,7 +460,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                               (__funnelshift_r(w3, w3, F.y) & 8u);
       return (F.y >> v) & 1u;
     } else {
-      const uint4 F = ldp<GC>(fns + f);
+      const uint4 F = h.fn_base == 0 ? ldp<GC>(fns + f) : fns_s[f];  // plan-uniform
       std::uint32_t v;
       if constexpr (RG) {
         v = gather4_shfl(wreg, F.z, F.w, 0);

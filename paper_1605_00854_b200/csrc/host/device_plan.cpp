@@ -251,6 +251,12 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     h.n_single_alias = gi + 1;
     arec.push_back(v.grp_fn_begin[gi] | (v.grp_alias_size[gi] << 24));
   }
+  // single-node rounds end on a 32-group boundary unless they cover the whole
+  // alias region, so the general path never sees a group below A1
+  if (h.n_single_alias < h.n_alias_groups) {
+    h.n_single_alias &= ~31u;
+    arec.resize(h.n_single_alias);
+  }
   if (arec.empty()) arec.push_back(0);
   auto record = [&](std::uint32_t f, std::uint32_t b) -> std::uint16_t {
     const std::uint32_t gc = v.fn_gather_count[f];
@@ -334,28 +340,79 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   }
 
   // compact records of the leading single-node groups for the register gather
-  // (n' <= 1023, at most 4 parents): sfn[f] = {rec0 | rec1 << 10 | rec2 << 20,
-  // rec3 | table << 16} with 10-bit records (word << 5 | rotation), and
-  // arec4[j] = {byte offset of the group's acell, byte offset of its sfn, N, ~N}
+  // (n' <= 1023, at most 4 parents), in a bank-column layout (dev_plan.h scol):
+  // group j owns 8-byte slot j % 16 of 128-byte rows, so the 16 lanes of each
+  // half-warp of a round read 16 distinct bank pairs. Per group, N rows each of
+  // U53 cells {alias, hi32(C)}, U32 cells {threshold, alias} and function
+  // records {rec0 | rec1 << 10 | rec2 << 20, rec3 | table << 16} (10-bit
+  // records word << 5 | rotation); arec4[j] = {byte offset of the U53 cells,
+  // byte offset of the function records, N, ~N}.
   h.single_compact = h.rg_ok && h.n_single_alias >= 32 && !h.single_gc5 ? 1u : 0u;
-  std::vector<std::uint32_t> sfn, arec4;
-  std::uint32_t n_sfn = 0;
+  std::vector<std::uint32_t> scol, arec4;
+  std::vector<std::uint32_t> scol_row0;  // per single group: first row
   if (h.single_compact) {
-    for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi)
-      n_sfn = std::max(n_sfn, v.grp_fn_begin[gi] + v.grp_alias_size[gi]);
-    sfn.assign(2 * static_cast<std::size_t>(n_sfn), 0);
-    for (std::uint32_t f = 0; f < n_sfn; ++f) {
-      const std::uint32_t gc = v.fn_gather_count[f];
-      if (gc > 4 || fn_members[f] != 1) throw model_error("compact single-node record misuse");
-      std::uint32_t rc[4];
-      for (std::uint32_t b = 0; b < 4; ++b) rc[b] = record(f, b) & 0x3FFu;
-      std::uint32_t table = 0;
-      for (std::uint32_t e = 0; e < (1u << gc); ++e)
-        table |= static_cast<std::uint32_t>(v.fn_tables[v.fn_table_begin[f] + e] & 1u) << e;
-      sfn[2 * f] = rc[0] | (rc[1] << 10) | (rc[2] << 20);
-      sfn[2 * f + 1] = rc[3] | (table << 16);
+    std::uint32_t rows[kScolSlots] = {};
+    scol_row0.resize(h.n_single_alias);
+    for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi) {
+      scol_row0[gi] = rows[gi % kScolSlots];
+      rows[gi % kScolSlots] += 3 * v.grp_alias_size[gi];
+    }
+    const std::uint32_t nrows = *std::max_element(rows, rows + kScolSlots);
+    scol.assign(static_cast<std::size_t>(nrows) * 2 * kScolSlots, 0);
+    auto put2 = [&](std::uint32_t row, std::uint32_t slot, std::uint32_t x, std::uint32_t y) {
+      const std::size_t w = (static_cast<std::size_t>(row) * kScolSlots + slot) * 2;
+      scol[w] = x;
+      scol[w + 1] = y;
+    };
+    for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi) {
+      const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
+      const std::uint32_t slot = gi % kScolSlots, r0 = scol_row0[gi];
+      for (std::uint32_t c = 0; c < asz; ++c) {
+        put2(r0 + c, slot, acell[4 * (ab + c) + 0], acell[4 * (ab + c) + 1]);
+        put2(r0 + asz + c, slot, acell[4 * (ab + c) + 2], acell[4 * (ab + c) + 3]);
+        const std::uint32_t f = v.grp_fn_begin[gi] + c;
+        const std::uint32_t gc = v.fn_gather_count[f];
+        if (gc > 4 || fn_members[f] != 1) throw model_error("compact single-node record misuse");
+        std::uint32_t rc[4];
+        for (std::uint32_t b = 0; b < 4; ++b) rc[b] = record(f, b) & 0x3FFu;
+        std::uint32_t table = 0;
+        for (std::uint32_t e = 0; e < (1u << gc); ++e)
+          table |= static_cast<std::uint32_t>(v.fn_tables[v.fn_table_begin[f] + e] & 1u) << e;
+        put2(r0 + 2 * asz + c, slot, rc[0] | (rc[1] << 10) | (rc[2] << 20), rc[3] | (table << 16));
+      }
     }
   }
+
+  // With the compact records the single-node groups' fns/acell entries are
+  // needed only by the fallback (non-compact) kernels: they move to an
+  // unstaged tail (fns_s, acell_s) and the staged fns/acell start at the first
+  // general group's entries (groups[].y/.z rebased).
+  h.fn_base = 0;
+  h.cell_base = 0;
+  if (h.single_compact) {
+    const std::uint32_t A1 = h.n_single_alias;
+    std::uint32_t fb = v.n_fns, cb = static_cast<std::uint32_t>(v.n_alias);
+    for (std::uint32_t gi = A1; gi < v.n_groups; ++gi) {
+      fb = std::min(fb, v.grp_fn_begin[gi]);
+      if (v.grp_alias_size[gi]) cb = std::min(cb, v.grp_alias_begin[gi]);
+    }
+    bool ok = true;
+    for (std::uint32_t gi = 0; gi < A1; ++gi)
+      ok = ok && v.grp_fn_begin[gi] + v.grp_alias_size[gi] <= fb &&
+           v.grp_alias_begin[gi] + v.grp_alias_size[gi] <= cb;
+    if (ok) {
+      h.fn_base = fb;
+      h.cell_base = cb;
+      for (std::uint32_t gi = 0; gi < v.n_groups; ++gi) {
+        groups[4 * gi + 1] = gi < A1 ? 0u : groups[4 * gi + 1] - fb;
+        groups[4 * gi + 2] = gi < A1 || v.grp_alias_size[gi] == 0 ? 0u : groups[4 * gi + 2] - cb;
+      }
+    }
+  }
+  std::vector<std::uint32_t> fns_s(fns.begin(), fns.begin() + 4 * static_cast<std::size_t>(h.fn_base));
+  std::vector<std::uint32_t> acell_s(acell.begin(), acell.begin() + 4 * static_cast<std::size_t>(h.cell_base));
+  fns.erase(fns.begin(), fns.begin() + 4 * static_cast<std::size_t>(h.fn_base));
+  acell.erase(acell.begin(), acell.begin() + 4 * static_cast<std::size_t>(h.cell_base));
 
   // ---- assemble
   std::size_t off = 0;
@@ -371,7 +428,7 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.off_grec = section(2 * grec.size());
   h.off_acell = section(4 * acell.size());
   h.off_arec = section(4 * arec.size());
-  h.off_sfn = section(4 * sfn.size());
+  h.off_scol = section(4 * scol.size());
   h.off_arec4 = section(16 * static_cast<std::size_t>(h.single_compact ? h.n_single_alias : 0));
   h.core_bytes = static_cast<std::uint32_t>(off);
   h.off_tables = section(tables.size());
@@ -382,7 +439,13 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   // FP64 cut-offs for the rare exact path: read through L1/L2, never staged
   h.off_acut = section(8 * acut.size());
   h.off_aidx = section(4 * aidx.size());
-  if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
+  if (h.fn_base || h.cell_base) {
+    h.off_fns_s = section(4 * fns_s.size());
+    h.off_acell_s = section(4 * acell_s.size());
+  } else {  // nothing moved: the fallback paths read the staged arrays
+    h.off_fns_s = h.off_fns;
+    h.off_acell_s = h.off_acell;
+  }
   if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
   ep.total_bytes = static_cast<std::uint32_t>(off);
   ep.blob.assign(off, 0);
@@ -394,14 +457,21 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   put(ep.blob, h.off_acut, acut);
   put(ep.blob, h.off_aidx, aidx);
   put(ep.blob, h.off_acell, acell);
+  if (h.fn_base || h.cell_base) {
+    put(ep.blob, h.off_fns_s, fns_s);
+    put(ep.blob, h.off_acell_s, acell_s);
+  }
   put(ep.blob, h.off_arec, arec);
-  put(ep.blob, h.off_sfn, sfn);
+  put(ep.blob, h.off_scol, scol);
   if (h.single_compact) {
     arec4.assign(4 * static_cast<std::size_t>(h.n_single_alias), 0);
+    auto addr = [&](std::uint32_t row, std::uint32_t slot) {
+      return h.off_scol + (row * kScolSlots + slot) * 8;
+    };
     for (std::uint32_t gi = 0; gi < h.n_single_alias; ++gi) {
-      const std::uint32_t asz = v.grp_alias_size[gi], base = v.grp_fn_begin[gi];
-      arec4[4 * gi + 0] = h.off_acell + 16 * v.grp_alias_begin[gi];
-      arec4[4 * gi + 1] = h.off_sfn + 8 * base;
+      const std::uint32_t asz = v.grp_alias_size[gi], slot = gi % kScolSlots, r0 = scol_row0[gi];
+      arec4[4 * gi + 0] = addr(r0, slot);
+      arec4[4 * gi + 1] = addr(r0 + 2 * asz, slot);
       arec4[4 * gi + 2] = asz;
       arec4[4 * gi + 3] = ~asz;
     }

@@ -60,6 +60,18 @@ def test_lanes_per_trajectory_invariance(pb, orc, cuda_ok, lpt):
     assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
 
 
+@pytest.mark.parametrize("lpt", [8, 16])
+def test_compact_plan_on_fallback_kernels(pb, orc, cuda_ok, lpt):
+    """A plan with compact single-node records (its single groups' general
+    records moved to the unstaged tail) run by the non-compact kernels."""
+    plan, pred = _setup(pb, "c2")
+    eng = pb.GpuEnsemble(plan, lanes_per_traj=lpt)
+    for stream in (0, 1):
+        st, cnt = eng.simulate(seed=13, n_traj=48, n_steps=200, pred=pred, stream=stream)
+        ost, ocnt = orc.simulate(plan.view, 13, 0, 48, 200, pred=pred, stream=stream)
+        assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+
+
 @pytest.mark.parametrize("placement", ["global", "core", "tables", "all"])
 def test_placement_invariance(pb, orc, cuda_ok, placement):
     plan, pred = _setup(pb, "c2")
