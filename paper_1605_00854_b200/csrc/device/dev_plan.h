@@ -82,6 +82,12 @@ inline constexpr bool kPhiloxPipeline = PBN_PHILOX_PIPELINE != 0;
 #ifndef PBN_COMPACT_SINGLE
 #define PBN_COMPACT_SINGLE 1
 #endif
+#ifndef PBN_QUAD_ROUNDS
+#define PBN_QUAD_ROUNDS 1
+#endif
+// four compact single-node rounds interleaved when a chunk holds four rounds
+// (U32: 4 draws per block; U53 would need two blocks per lane, which costs more)
+inline constexpr bool kQuadRounds = PBN_QUAD_ROUNDS != 0;
 inline constexpr bool kUseCompactSingle = PBN_COMPACT_SINGLE != 0;  // GM = 2 when the plan allows
 inline constexpr std::uint32_t kA53MaxCells = 2048;
 inline constexpr std::uint32_t kScolSlots = 16;          // 8-byte slots per 128-byte row           // alias fits the low 11 bits

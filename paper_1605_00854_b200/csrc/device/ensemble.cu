@@ -615,6 +615,29 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t t = 0; t < DPB * CB; t += 2) {
           const std::uint32_t jr0 = j0 + t * LPT, jr1 = jr0 + LPT;
           if (jr0 >= A) break;
+          if constexpr (kQuadRounds && SC && DPB * CB >= 4) {
+            // four single-node rounds at once: four independent chains
+            if ((t & 3) == 0 && jr0 + 4 * LPT <= A1) {
+              bool rr[4];
+              std::uint32_t f[4];
+#pragma unroll
+              for (std::uint32_t u = 0; u < 4; ++u) f[u] = single_fn(jr0 + u * LPT + r, (t + u) * LPT + r, rr[u]);
+              if constexpr (STREAM == STREAM_U53) {
+                if (__builtin_expect(rr[0] || rr[1] || rr[2] || rr[3], 0)) {
+#pragma unroll
+                  for (std::uint32_t u = 0; u < 4; ++u)
+                    if (rr[u]) f[u] = single_fn_exact(jr0 + u * LPT + r, (t + u) * LPT + r);
+                }
+              }
+              bool b[4];
+#pragma unroll
+              for (std::uint32_t u = 0; u < 4; ++u) b[u] = single_out(Sc, wreg, f[u]);
+#pragma unroll
+              for (std::uint32_t u = 0; u < 4; ++u) store_bits(Sn, jr0 + u * LPT, __ballot_sync(smask, b[u]), true);
+              t += 2;  // with the loop's += 2: next quad
+              continue;
+            }
+          }
           if (jr1 + LPT <= A1) {
             bool rare0, rare1;
             std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
