@@ -46,8 +46,9 @@ class Workload:
 
 
 CONFIGS = {
-    "c1": Workload("c1", 100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 4096, 1_000_000,
-                   note="n=100, target node0=1 AND node1=1; CPU ref 1 traj x 1e6 steps"),
+    "c1": Workload("c1", 100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605, 131072, 100_000,
+                   note="n=100, target node0=1 AND node1=1; CPU ref 1 traj x 1e6 steps; "
+                        "GPU: 131072 trajectories x 1e5 steps per bench step"),
     "c2": Workload("c2", 1000, (1, 5), (1, 4), 0.001, 0.0, 3, False, 1606, 4096, 100_000,
                    k_max=16, note="n=1000, 4096 trajectories x 1e5 steps, single B200 (headline)"),
     "c3": Workload("c3", 96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607, 65536, 0,

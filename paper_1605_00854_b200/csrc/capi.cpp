@@ -26,6 +26,14 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches);
+cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
+                                 int stream_kind, std::uint32_t warps_per_cta,
+                                 const dev_run_params& rp, std::uint64_t* d_states,
+                                 std::uint64_t* d_counts, cudaStream_t stream,
+                                 std::uint32_t* launches);
+bool lane_kernel_fits(const dev_plan_header& h);
+std::uint32_t lane_max_warps();
+std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
                               std::uint32_t n, cudaStream_t stream);
 cudaError_t launch_series_stats(const std::uint32_t* d_series, std::uint32_t n_traj,
@@ -104,7 +112,12 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 
 // Lanes per trajectory: by network size, then doubled until the ensemble
 // gives ~24 resident warps per SM (latency hiding) or one warp per trajectory.
+// Lane-per-trajectory kernel (lane_ensemble.cu) for networks up to 255 kept
+// nodes once the ensemble gives >= 10 warps of 32 trajectories per SM
+// (measured on c1/c3: 2.1-2.2x over sub-warps at 131072 trajectories, behind
+// them below ~40000).
 std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t sms) {
+  if (n_kept <= 255 && n_traj >= static_cast<std::uint64_t>(sms) * 320) return 1;
   std::uint32_t lpt = n_kept <= 256 ? 8 : n_kept <= 512 ? 16 : 32;
   while (lpt < 32 && n_traj * lpt / 32 < static_cast<std::uint64_t>(sms) * 24) lpt *= 2;
   return lpt;
@@ -124,6 +137,16 @@ std::uint32_t staged_bytes(const pbn_gpu& g) { return staged_bytes_at(g.ep.h, g.
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
 std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt,
                          bool node_counts) {
+  if (lpt == 1 && lane_kernel_fits(g.ep.h)) {  // lane kernel: 32 trajectories per warp
+    const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) + 31) / 32;
+    std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
+    w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lane_max_warps(), w));
+    const std::uint64_t per_warp = lane_warp_words(g.ep.h, node_counts) * 4;
+    const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
+    while (w > 1 && w * per_warp > avail) --w;
+    if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
+    return static_cast<std::uint32_t>(w);
+  }
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? 28 : 32, w));
@@ -198,9 +221,12 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
     }
   }
   g.launches = 0;
-  const cudaError_t e = launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream),
-                                        g.last_lpt, g.last_warps, rp, d_states, d_counts, stream,
-                                        &g.launches);
+  const cudaError_t e =
+      g.last_lpt == 1 && lane_kernel_fits(g.ep.h)
+          ? launch_lane_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream),
+                                 g.last_warps, rp, d_states, d_counts, stream, &g.launches)
+          : launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_lpt,
+                            g.last_warps, rp, d_states, d_counts, stream, &g.launches);
   g.place = place0;
   ck(e, "ensemble launch");
 }

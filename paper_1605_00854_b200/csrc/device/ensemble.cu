@@ -25,141 +25,9 @@
 #include <cstdint>
 #include <type_traits>
 
-#include "dev_plan.h"
-#include "philox.cuh"
+#include "kernel_common.cuh"
 
 namespace pbn_b200 {
-
-enum { STREAM_U53 = 0, STREAM_U32 = 1 };
-// Plan placement = the staged prefix of the blob (dev_plan.h): 0 nothing (all
-// reads through the read-only L1/L2 path), 1 core, 2 core + tables, 3 also the
-// perturbation cells of the launch's stream.
-enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_TABLES = 2, PLACE_ALL = 3 };
-
-template <int STREAM>
-__host__ __device__ inline std::uint32_t staged_prefix(const dev_plan_header& h, int place) {
-  if (place == PLACE_ALL) return STREAM == 0 ? h.blob_bytes : h.off_pert53;
-  if (place == PLACE_TABLES) return h.off_pert32;
-  if (place == PLACE_CORE) return h.core_bytes;
-  return 0;
-}
-
-template <bool G, class T>
-__device__ __forceinline__ T ldp(const T* p) {
-  if constexpr (G)
-    return __ldg(p);
-  else
-    return *p;
-}
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// Stage `bytes` (multiple of 16) from global to shared memory with bulk
-// copies completing on one mbarrier; every thread of the CTA waits.
-__device__ __forceinline__ void stage_plan(std::uint8_t* dst, const std::uint8_t* src,
-                                           std::uint32_t bytes, std::uint64_t* bar) {
-  const std::uint32_t b = smem_u32(bar);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-                 : "memory");
-    for (std::uint32_t off = 0; off < bytes; off += 32768u) {
-      const std::uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-              "r"(smem_u32(dst + off)),
-          "l"(src + off), "r"(n), "r"(b)
-          : "memory");
-    }
-  }
-  __syncthreads();
-  std::uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(b)
-        : "memory");
-  }
-}
-
-template <int STREAM>
-struct draws {
-  static constexpr std::uint32_t kPerBlock = STREAM == STREAM_U53 ? 2 : 4;
-};
-
-// Raw draw e of a Philox block: r53 as (hi32, lo21) pieces for U53, r32 for U32.
-struct raw53 {
-  std::uint32_t hi;  // bits [21, 53) of r53  (= x[2e+1])
-  std::uint32_t lo;  // x[2e]; bits [0, 21) of r53 are lo >> 11
-  __device__ __forceinline__ std::uint64_t value() const {
-    return (static_cast<std::uint64_t>(hi) << 21) | (lo >> 11);
-  }
-  // raw word R = hi << 32 | lo; r53 = R >> 11 (dev_plan.h: raw-word thresholds)
-  __device__ __forceinline__ std::uint64_t raw() const {
-    return (static_cast<std::uint64_t>(hi) << 32) | lo;
-  }
-};
-
-__device__ __forceinline__ raw53 pick53(const uint4& x, std::uint32_t e) {
-  return e == 0 ? raw53{x.y, x.x} : raw53{x.w, x.z};
-}
-__device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e) {
-  return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
-}
-
-// Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form on
-// the raw draw word: the cell index is the top k bits, the threshold compare
-// runs on the remaining 64-k bits (dev_plan.h pert53).
-template <bool G>
-__device__ __forceinline__ std::uint32_t pert_draw53(const std::uint64_t* cells, raw53 r,
-                                                     std::uint32_t k) {
-  const std::uint32_t c = r.hi >> (32 - k);
-  const std::uint32_t hmask = 0xFFFFFFFFu >> k;
-  const std::uint64_t e = ldp<G>(cells + c);
-  const std::uint32_t ehi = static_cast<std::uint32_t>(e >> 32);
-  const std::uint64_t rl = (static_cast<std::uint64_t>(r.hi & hmask) << 32) | r.lo;
-  const std::uint64_t el = (static_cast<std::uint64_t>(ehi & hmask) << 32) | static_cast<std::uint32_t>(e);
-  return rl < el ? c : (ehi >> (32 - k));
-}
-
-template <bool G>
-__device__ __forceinline__ std::uint32_t pert_draw32(const std::uint32_t* cells, std::uint32_t r,
-                                                     std::uint32_t k) {
-  const std::uint32_t c = r >> (32 - k);
-  const std::uint32_t lmask = (1u << (32 - k)) - 1;
-  const std::uint32_t e = ldp<G>(cells + c);
-  return (r & lmask) < (e & lmask) ? c : (e >> (32 - k));
-}
-
-// Gather 4 parent bits (records r0..r3 packed in two words) into slots b0..b0+3.
-__device__ __forceinline__ std::uint32_t gather4(const std::uint32_t* S, std::uint32_t p01,
-                                                 std::uint32_t p23, std::uint32_t b0) {
-  const std::uint32_t r0 = p01 & 0xFFFFu, r1 = p01 >> 16, r2 = p23 & 0xFFFFu, r3 = p23 >> 16;
-  const std::uint32_t w0 = S[r0 >> 5], w1 = S[r1 >> 5], w2 = S[r2 >> 5], w3 = S[r3 >> 5];
-  return (__funnelshift_r(w0, w0, r0) & (1u << b0)) | (__funnelshift_r(w1, w1, r1) & (2u << b0)) |
-         (__funnelshift_r(w2, w2, r2) & (4u << b0)) | (__funnelshift_r(w3, w3, r3) & (8u << b0));
-}
-
-// Same, with the state held one word per lane (n' <= 1023, LPT = 32): the
-// parent word comes from a shuffle (the source lane index is taken mod 32, so
-// the packed record needs no masking) instead of a shared-memory load.
-__device__ __forceinline__ std::uint32_t gather4_shfl(std::uint32_t wreg, std::uint32_t p01,
-                                                      std::uint32_t p23, std::uint32_t b0) {
-  const std::uint32_t w0 = __shfl_sync(0xFFFFFFFFu, wreg, p01 >> 5);
-  const std::uint32_t w1 = __shfl_sync(0xFFFFFFFFu, wreg, p01 >> 21);
-  const std::uint32_t w2 = __shfl_sync(0xFFFFFFFFu, wreg, p23 >> 5);
-  const std::uint32_t w3 = __shfl_sync(0xFFFFFFFFu, wreg, p23 >> 21);
-  return (__funnelshift_r(w0, w0, p01) & (1u << b0)) |
-         (__funnelshift_r(w1, w1, p01 >> 16) & (2u << b0)) |
-         (__funnelshift_r(w2, w2, p23) & (4u << b0)) |
-         (__funnelshift_r(w3, w3, p23 >> 16) & (8u << b0));
-}
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.

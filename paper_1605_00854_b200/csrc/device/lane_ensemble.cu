@@ -1,0 +1,417 @@
+// Lane-per-trajectory ensemble kernel for small networks: the same step as
+// ensemble.cu (the reference's grouped_simulator::step, engine.hpp:255-312,
+// driven by simulate(), engine.hpp:371-384), bit-exact on the same injected
+// stream, with one whole trajectory per lane.
+//
+// Why: a small network (c1: n' = 77, c3: n' = 65) has a handful of phase-A
+// Philox blocks and ~30 groups, so a sub-warp per trajectory leaves most lanes
+// idle or pays sub-warp ballots/atomics per round. Here every lane runs the
+// reference's sequential group loop for its own trajectory:
+//
+//   * the group loop is warp-uniform (same plan, same group order), so the
+//     group record, its entry width and its output offset are broadcast
+//     reads; only the chosen combined function and the parent values differ
+//     per lane;
+//   * states live in shared memory in a [word][32 lanes] layout: the parent
+//     gathers and the output ORs of 32 lanes touch 32 distinct banks;
+//   * phase-B draws come straight from the lane's own Philox block in
+//     registers (one block per DPB alias groups, at warp-uniform points).
+//
+// The function phase runs under divergence (lanes whose step short-circuits
+// sit it out), so this layout pays when the ensemble is large (>= ~16 warps
+// per SM) and the network small; the host picks it as lanes_per_traj = 1.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "kernel_common.cuh"
+
+namespace pbn_b200 {
+
+// The exact FP64 choice of engine.hpp:285-290 (boundary draws, forced FP64
+// runs, groups beyond the integer cells). Out of line so the compiler cannot
+// hoist it into the fast path.
+__device__ __noinline__ std::uint32_t alias_exact_fp64(const double* __restrict__ acut,
+                                                       const std::uint32_t* __restrict__ aidx,
+                                                       std::uint32_t asz, std::uint32_t ab,
+                                                       std::uint64_t r53) {
+  const double u = __ull2double_rn(r53) * 0x1.0p-53;
+  const double xx = __dmul_rn(u, __uint2double_rn(asz));
+  std::uint32_t c = __double2uint_rz(xx);
+  if (c >= asz) c = asz - 1;
+  const double fr = __dsub_rn(xx, __uint2double_rn(c));
+  return fr < __ldg(acut + ab + c) ? c : __ldg(aidx + ab + c);
+}
+
+constexpr int kLaneMaxWarps = 28;  // 896 threads: 72 registers per thread
+
+template <int STREAM, int PLACE>
+__global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
+    pbn_lane_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
+                    const dev_run_params rp, std::uint64_t* __restrict__ states,
+                    std::uint64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) std::uint8_t smem[];
+  __shared__ std::uint64_t stage_bar;
+  constexpr bool GC = PLACE < PLACE_CORE;
+  constexpr bool GT = PLACE < PLACE_TABLES;
+  constexpr bool GP = PLACE < PLACE_ALL;
+  constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
+
+  const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
+  if (staged) stage_plan(smem, gblob, staged, &stage_bar);
+
+  const std::uint8_t* core = GC ? gblob : smem;
+  const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
+  const std::uint8_t* pbase = GP ? gblob : smem;
+  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pbase + h.off_pert53);
+  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pbase + h.off_pert32);
+  const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
+  const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
+  const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
+  const double* acut = reinterpret_cast<const double*>(gblob + h.off_acut);
+  const std::uint32_t* aidx = reinterpret_cast<const std::uint32_t*>(gblob + h.off_aidx);
+  const uint4* acell = reinterpret_cast<const uint4*>(core + h.off_acell);
+  const std::uint8_t* sbase = (h.fn_base || h.cell_base) ? gblob : core;
+  const uint4* fns_s = reinterpret_cast<const uint4*>(sbase + h.off_fns_s);
+  const uint4* acell_s = reinterpret_cast<const uint4*>(sbase + h.off_acell_s);
+  const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
+
+  const std::uint32_t lane = threadIdx.x & 31;
+  const std::uint32_t warp = threadIdx.x >> 5;
+  const std::uint64_t tloc = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tloc >= rp.n_traj) return;
+
+  // per-warp shared memory: two state buffers of sw32 words x 32 lanes, then
+  // (node counts) 8 counter planes per word; lane columns
+  const std::uint32_t sw32 = h.sw32;
+  const std::uint32_t warp_words = (2 + (rp.node_counts ? 8u : 0u)) * sw32 * 32;
+  std::uint32_t* wbuf = reinterpret_cast<std::uint32_t*>(smem + staged) +
+                        static_cast<std::size_t>(warp) * warp_words + lane;
+  std::uint32_t* planes = wbuf + 2 * sw32 * 32;  // plane i of word w at [(8w + i) * 32]
+  std::uint32_t cur = 0;                          // current state buffer (per lane)
+  {
+    const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
+    for (std::uint32_t w = 0; w < sw32; ++w) wbuf[32 * w] = src[w];
+    if (rp.node_counts)
+      for (std::uint32_t i = 0; i < 8 * sw32; ++i) planes[32 * i] = 0;
+  }
+
+  const std::uint32_t k = h.k, g = h.g;
+  const bool exact_all = rp.exact_alias != 0;
+  const std::uint32_t nb0 = (g + h.has_leaf + DPB - 1) / DPB;  // blocks of phase A
+  const std::uint32_t A = h.n_alias_groups, NG = h.n_groups, A1 = h.n_single_alias;
+  const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
+  std::uint32_t thi0, tlo0;
+  mulhilo(kPhiloxM0, traj, thi0, tlo0);
+
+  auto pred_eval = [&](const std::uint32_t* S) -> std::uint32_t {
+    bool ok = rp.pred.n != 0;
+    for (std::uint32_t i = 0; i < rp.pred.n; ++i)
+      ok = ok && (S[32 * rp.pred.w[i]] & rp.pred.mask[i]) == rp.pred.want[i];
+    return ok ? 1u : 0u;
+  };
+
+  // Combined-function choice (engine.hpp:284-291) from raw draw x: U53 integer
+  // cells with the rare FP64 path, U32 integer cells (dev_plan.h acell).
+  auto alias_fast = [&](const uint4* cells, std::uint32_t asz, std::uint32_t ab, const raw53& r,
+                        std::uint32_t r32, bool& rare) -> std::uint32_t {
+    if constexpr (STREAM == STREAM_U53) {
+      const std::uint64_t P = static_cast<std::uint64_t>(r.hi) * asz;
+      const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
+      const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + e));
+      rare = rare || static_cast<std::uint32_t>(P) > ~asz || r.hi == V.y;
+      return r.hi < V.y ? e : V.x;
+    } else {
+      const std::uint64_t P = static_cast<std::uint64_t>(r32) * asz;
+      const std::uint32_t c = static_cast<std::uint32_t>(P >> 32);
+      const uint2 cell = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + c) + 1);
+      return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
+    }
+  };
+  auto gather_fn = [&](const std::uint32_t* S, const uint4& F) -> std::uint32_t {
+    const std::uint32_t gc = F.y & 31u;
+    std::uint32_t v = gather4_col(S, F.z, F.w, 0);
+    if (gc > 4) {
+      const std::uint32_t xq = F.y >> 8;
+      for (std::uint32_t q = 4; q < gc; q += 4) {
+        const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+        v |= gather4_col(S, rr.x, rr.y, q);
+      }
+    }
+    return v;
+  };
+
+  std::uint32_t nc_pending = 0;
+  auto nc_flush = [&]() {
+    std::uint64_t* dst = rp.node_counts + tloc * h.n_kept;
+    for (std::uint32_t w = 0; w < sw32; ++w) {
+      std::uint32_t pl[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pl[i] = planes[32 * (8 * w + i)];
+        planes[32 * (8 * w + i)] = 0;
+      }
+      for (std::uint32_t b = 0; b < 32; ++b) {
+        const std::uint32_t node = 32 * w + b;
+        if (node >= h.n_kept) break;
+        std::uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c |= ((pl[i] >> b) & 1u) << i;
+        if (c) dst[node] += c;
+      }
+    }
+    nc_pending = 0;
+  };
+
+  const std::uint32_t z0 = pred_eval(wbuf);
+  std::uint32_t prev = 2u, kphase = 0;
+  if (rp.thin_mode == 0) prev = z0;
+  if (rp.thin_mode == 1 && rp.tprev) {
+    const std::uint32_t tp = rp.tprev[tloc];
+    prev = tp & 3u;
+    kphase = tp >> 2;
+  }
+  std::uint32_t nv = 0, np1 = 0, nh1 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
+  std::uint32_t* ser = rp.series ? rp.series + tloc * rp.series_stride : nullptr;
+  std::uint32_t sword = 0;
+  if (ser && rp.series_init && rp.series_bit0 > 0 && z0) {
+    const std::uint64_t p0 = rp.series_bit0 - 1;
+    ser[p0 >> 5] |= 1u << (p0 & 31);
+  }
+  const std::uint64_t s_end = rp.step_begin + rp.n_steps;
+
+  for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
+    std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
+    const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+
+    // ---- phase A: draws 0..g (engine.hpp:257-268)
+    bool flip = false, leaf = false;
+    auto phase_a = [&](auto bern_c) {
+      constexpr bool BERN = decltype(bern_c)::value;  // node-wise plans (Method_old / reduction)
+      for (std::uint32_t b = 0; b < nb0; ++b) {
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+        const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) {
+          std::uint32_t c;
+          if constexpr (BERN) {
+            if constexpr (STREAM == STREAM_U53)
+              c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
+            else
+              c = pick32(x, e) < h.pthr32 ? 1u : 0u;
+          } else if constexpr (STREAM == STREAM_U53) {
+            c = pert_draw53<GP>(pert53, pick53(x, e), k);
+          } else {
+            c = pert_draw32<GP>(pert32, pick32(x, e), k);
+          }
+          const int q = rem - 1 - static_cast<int>(e);
+          c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+          if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+            flip = true;
+            const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
+            Sc[32 * w] ^= c << sh;
+            if (sh != 0 && (c >> (32 - sh)) != 0) Sc[32 * (w + 1)] ^= c >> (32 - sh);
+          }
+          if (q == -1 && h.has_leaf) {
+            if constexpr (STREAM == STREAM_U53)
+              leaf = pick53(x, e).raw() > h.leaf_thr53;
+            else
+              leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
+          }
+        }
+      }
+    };
+    if (h.pert_mode != 0)
+      phase_a(std::true_type{});
+    else
+      phase_a(std::false_type{});
+
+    if (flip) {
+      ++npert;
+    } else if (!leaf) {
+      // ---- function phase: the reference's group loop (engine.hpp:270-311)
+      std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
+      for (std::uint32_t w = 0; w < sw32; ++w) Sn[32 * w] = 0;
+      uint4 xb = make_uint4(0, 0, 0, 0);  // the phase-B block holding draw j
+      for (std::uint32_t gi = 0; gi < NG; ++gi) {
+        raw53 r{0, 0};
+        std::uint32_t r32 = 0;
+        if (gi < A) {  // draw j = gi (alias groups come first)
+          const std::uint32_t e = gi % DPB;
+          if (e == 0) xb = philox_block(sp, nb0 + gi / DPB, rp.rk0, rp.rk1);
+          if constexpr (STREAM == STREAM_U53)
+            r = pick53(xb, e);
+          else
+            r32 = pick32(xb, e);
+        }
+        std::uint32_t olo, ohi = 0, off, members;
+        if (gi < A1) {  // single node at offset gi, inline 1-bit tables (dev_plan.h arec)
+          const std::uint32_t ar = ldp<GC>(arec + gi);
+          const std::uint32_t base = ar & 0xFFFFFFu, asz = ar >> 24;
+          bool rare = exact_all;
+          // plan-uniform branches keep each load in one address space
+          std::uint32_t f = base + (h.cell_base == 0 ? alias_fast(acell, asz, base, r, r32, rare)
+                                                     : alias_fast(acell_s, asz, base, r, r32, rare));
+          if constexpr (STREAM == STREAM_U53)
+            if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r.value());
+          uint4 F;
+          if (h.fn_base == 0)
+            F = ldp<GC>(fns + f);
+          else
+            F = fns_s[f];
+          olo = (F.x >> gather_fn(Sc, F)) & 1u;
+          off = gi;
+          members = 1;
+        } else {
+          const uint4 G = ldp<GC>(groups + gi);
+          const std::uint32_t asz = G.w & 0x7FFFFFu;
+          members = (G.w >> 24) + 1;
+          off = G.x;
+          std::uint32_t idx = 0;
+          if (asz != 0) {
+            bool rare = exact_all || (G.w & kGroupExactAlias);
+            idx = alias_fast(acell, asz, G.z, r, r32, rare);
+            if constexpr (STREAM == STREAM_U53)
+              if (__builtin_expect(rare, 0)) idx = alias_exact_fp64(acut, aidx, asz, G.z + h.cell_base, r.value());
+          }
+          const uint4 F = ldp<GC>(fns + G.y + idx);
+          const std::uint32_t v = gather_fn(Sc, F);
+          if (F.y & 0x80u) {  // inline table
+            const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
+            olo = (F.x >> (v * members)) & m;
+          } else {
+            const std::uint32_t el2 = (F.y >> 5) & 3u;
+            if (el2 == 0) {
+              olo = ldp<GT>(tab + F.x + v);
+            } else if (el2 == 1) {
+              olo = ldp<GT>(reinterpret_cast<const std::uint16_t*>(tab + F.x) + v);
+            } else if (el2 == 2) {
+              olo = ldp<GT>(reinterpret_cast<const std::uint32_t*>(tab + F.x) + v);
+            } else {
+              const uint2 o = ldp<GT>(reinterpret_cast<const uint2*>(tab + F.x) + v);
+              olo = o.x;
+              ohi = o.y;
+            }
+          }
+        }
+        // next |= out << offset (engine.hpp:304-309); offset and width are
+        // the group's, so the branches are warp-uniform
+        const std::uint32_t w = off >> 5, sh = off & 31;
+        Sn[32 * w] |= olo << sh;
+        if (sh + members > 32) {
+          Sn[32 * (w + 1)] |= sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
+          if (sh + members > 64) Sn[32 * (w + 2)] |= ohi >> (32 - sh);
+        }
+      }
+      cur ^= 1;
+      Sc = Sn;
+      ++nfn;
+    }
+
+    // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
+    const std::uint32_t hit = pred_eval(Sc);
+    nhit += hit;
+    if (++kphase == rp.kappa) {
+      kphase = 0;
+      const std::uint32_t valid = (prev >> 1) ^ 1u;
+      nv += valid;
+      np1 += prev & 1u;
+      nh1 += hit & valid;
+      n11 += prev & hit;
+      prev = hit;
+    }
+    if (rp.node_counts) {  // launch-uniform branch
+      for (std::uint32_t w = 0; w < sw32; ++w) {
+        std::uint32_t x = Sc[32 * w];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const std::uint32_t p = planes[32 * (8 * w + i)];
+          planes[32 * (8 * w + i)] = p ^ x;
+          x &= p;
+        }
+      }
+      if (++nc_pending == 255) nc_flush();
+    }
+    if (ser != nullptr) {
+      const std::uint64_t pos = rp.series_bit0 + (s - rp.step_begin);
+      sword |= hit << (pos & 31);
+      if ((pos & 31) == 31 || s + 1 == s_end) {
+        if (sword) ser[pos >> 5] |= sword;
+        sword = 0;
+      }
+    }
+  }
+  if (rp.node_counts && nc_pending) nc_flush();
+  if (rp.tprev) rp.tprev[tloc] = static_cast<std::uint8_t>(prev | (kphase << 2));
+  {
+    const std::uint32_t* Sf = wbuf + cur * (sw32 * 32);
+    std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(states + tloc * (sw32 / 2));
+    for (std::uint32_t w = 0; w < sw32; ++w) dst[w] = Sf[32 * w];
+  }
+  std::uint64_t* c = counts + tloc * 8;
+  const bool pr = rp.pred.n != 0;
+  c[0] = rp.n_steps;
+  c[1] = pr ? nhit : 0;
+  c[2] = pr ? nv - np1 - nh1 + n11 : 0;
+  c[3] = pr ? nh1 - n11 : 0;
+  c[4] = pr ? np1 - n11 : 0;
+  c[5] = pr ? n11 : 0;
+  c[6] = nfn;
+  c[7] = npert;
+}
+
+using lane_kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
+                                std::uint64_t*, std::uint64_t*);
+
+template <int STREAM>
+lane_kernel_fn pick_lane_place(int place) {
+  switch (place) {
+    case PLACE_ALL:
+      return pbn_lane_kernel<STREAM, PLACE_ALL>;
+    case PLACE_TABLES:
+      return pbn_lane_kernel<STREAM, PLACE_TABLES>;
+    case PLACE_CORE:
+      return pbn_lane_kernel<STREAM, PLACE_CORE>;
+    default:
+      return pbn_lane_kernel<STREAM, PLACE_GLOBAL>;
+  }
+}
+
+// The lane kernel serves lanes_per_traj = 1 for networks up to 255 kept nodes
+// (8 state words; larger ones use ensemble.cu's one-lane sub-warps).
+bool lane_kernel_fits(const dev_plan_header& h) { return h.sw32 <= 8; }
+std::uint32_t lane_max_warps() { return kLaneMaxWarps; }
+
+// Shared-memory words per warp of the lane kernel: two state buffers and the
+// optional counter planes, sw32 words per lane each.
+std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts) {
+  return static_cast<std::size_t>(2 + (node_counts ? 8 : 0)) * h.sw32 * 32;
+}
+
+cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
+                                 int stream_kind, std::uint32_t warps_per_cta,
+                                 const dev_run_params& rp, std::uint64_t* d_states,
+                                 std::uint64_t* d_counts, cudaStream_t stream,
+                                 std::uint32_t* launches) {
+  const lane_kernel_fn fn = stream_kind == STREAM_U53 ? pick_lane_place<STREAM_U53>(place)
+                                                      : pick_lane_place<STREAM_U32>(place);
+  const std::uint32_t threads = warps_per_cta * 32;
+  const std::uint32_t grid = (rp.n_traj + threads - 1) / threads;
+  const std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
+                                                      : staged_prefix<STREAM_U32>(h, place);
+  const std::size_t smem = staged +
+                           static_cast<std::size_t>(warps_per_cta) *
+                               lane_warp_words(h, rp.node_counts != nullptr) * 4 +
+                           16;
+  cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  if (grid == 0) return cudaSuccess;
+  fn<<<grid, threads, smem, stream>>>(h, d_blob, rp, d_states, d_counts);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace pbn_b200
