@@ -213,8 +213,10 @@ int pbn_device_count(int* count);
 int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lanes_per_traj,
                    pbn_gpu** out);
 /* Force where the plan lives: 0 auto, 1 global (L1/L2), 2 core in smem, 3 core +
- * truth tables in smem, 4 everything (incl. perturbation cells) in smem.
- * PBN_ERESOURCE if it does not fit. */
+ * truth tables in smem, 4 everything (incl. perturbation cells) in smem, 5 core +
+ * the perturbation cells in smem (tables through L1/L2).
+ * PBN_ERESOURCE if it does not fit. pbn_gpu_info reports the level as
+ * (placement code - 1): 0 global, 1 core, 2 tables, 3 all, 4 core + cells. */
 int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement);
 int pbn_gpu_info(const pbn_gpu* g, uint32_t* lanes_per_traj, uint32_t* tables_in_smem,
                  uint64_t* smem_bytes, uint64_t* plan_bytes, uint32_t* warps_per_cta);

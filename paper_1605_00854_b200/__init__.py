@@ -497,7 +497,7 @@ class GpuEnsemble:
 
     def set_placement(self, placement: str) -> None:
         """'auto' | 'global' | 'core' | 'tables' | 'all' (staged prefix of the plan)."""
-        code = {"auto": 0, "global": 1, "core": 2, "tables": 3, "all": 4}[placement]
+        code = {"auto": 0, "global": 1, "core": 2, "tables": 3, "all": 4, "core_pert": 5}[placement]
         _check(lib.pbn_gpu_set_placement(self._h, code))
 
     def info(self):
@@ -505,7 +505,7 @@ class GpuEnsemble:
         sm, pb = C.c_uint64(), C.c_uint64()
         _check(lib.pbn_gpu_info(self._h, C.byref(lpt), C.byref(place), C.byref(sm), C.byref(pb),
                                 C.byref(wpc)))
-        return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "tables", "all")[place.value],
+        return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "tables", "all", "core_pert")[place.value],
                 "staged_smem_bytes": sm.value, "plan_bytes": pb.value,
                 "warps_per_cta": wpc.value}
 

@@ -126,12 +126,24 @@ std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t
 // Staged prefix of the blob for a placement level (dev_plan.h); level 3
 // counts both perturbation tables (the launch stages its stream's only).
 std::uint32_t staged_bytes_at(const dev_plan_header& h, int place) {
+  if (place == 4)  // core + the larger stream's perturbation cells
+    return h.core_bytes + std::max(h.blob_bytes - h.off_pert53, h.off_pert53 - h.off_pert32);
   if (place == 3) return h.blob_bytes;
   if (place == 2) return h.off_pert32;
   if (place == 1) return h.core_bytes;
   return 0;
 }
 std::uint32_t staged_bytes(const pbn_gpu& g) { return staged_bytes_at(g.ep.h, g.place); }
+
+// Placement levels from most to least shared memory: all, tables, core +
+// perturbation cells, core, global (run_device steps down this order when
+// the ensemble's state does not fit next to the staged plan).
+constexpr int kPlaceOrder[] = {3, 2, 4, 1, 0};
+int next_lower_place(int place) {
+  for (int i = 0; i + 1 < 5; ++i)
+    if (kPlaceOrder[i] == place) return kPlaceOrder[i + 1];
+  return 0;
+}
 
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
@@ -217,7 +229,7 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
         g.place = place0;
         throw;
       }
-      --g.place;
+      g.place = next_lower_place(g.place);
     }
   }
   g.launches = 0;
@@ -477,8 +489,8 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
     g->sms = static_cast<uint32_t>(sms);
     const dev_plan_header& h = g->ep.h;
     g->place = 0;
-    for (int lvl = 3; lvl >= 1; --lvl)
-      if (staged_bytes_at(h, lvl) + kStateReserve <= g->smem_optin) {
+    for (int lvl : kPlaceOrder)
+      if (lvl != 0 && staged_bytes_at(h, lvl) + kStateReserve <= g->smem_optin) {
         g->place = lvl;
         break;
       }
@@ -492,9 +504,10 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
 int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement) {
   return guard([&] {
     need(g, "gpu");
-    if (placement > 4) throw std::invalid_argument("placement must be 0..4");
+    if (placement > 5) throw std::invalid_argument("placement must be 0..5");
     if (placement == 0) return;
-    const int want = static_cast<int>(placement) - 1;  // 0 global, 1 core, 2 +tables, 3 all
+    // 0 global, 1 core, 2 +tables, 3 all, 4 core + perturbation cells
+    const int want = static_cast<int>(placement) - 1;
     const std::uint64_t need_bytes = staged_bytes_at(g->ep.h, want);
     if (need_bytes + 4096 > g->smem_optin)
       throw resource_error("requested placement does not fit in shared memory");

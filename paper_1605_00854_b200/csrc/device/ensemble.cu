@@ -29,6 +29,11 @@
 
 namespace pbn_b200 {
 
+#ifndef PBN_GENERAL_PAIRS
+#define PBN_GENERAL_PAIRS 1
+#endif
+constexpr bool kGeneralPairs = PBN_GENERAL_PAIRS != 0;
+
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
 constexpr int kMaxWarpsLpt32 = 28;
@@ -42,21 +47,20 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                         std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
-  constexpr bool GC = PLACE < PLACE_CORE;    // core sections read from global
-  constexpr bool GT = PLACE < PLACE_TABLES;   // tables read from global
-  constexpr bool GP = PLACE < PLACE_ALL;      // perturbation cells read from global
+  constexpr bool GC = placement<PLACE>::global_core;    // core sections read from global
+  constexpr bool GT = placement<PLACE>::global_tables;  // tables read from global
+  constexpr bool GP = placement<PLACE>::global_pert;    // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
   constexpr bool RG = GM >= 1;
   constexpr bool SC = GM == 2;
 
-  const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
-  if (staged) stage_plan(smem, gblob, staged, &stage_bar);
+  const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
-  const std::uint8_t* pbase = GP ? gblob : smem;
-  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pbase + h.off_pert53);
-  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pbase + h.off_pert32);
+  const std::uint8_t* pcells = pert_cells<STREAM, PLACE>(smem, gblob, h);
+  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pcells);
+  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pcells);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
@@ -300,8 +304,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     } else {
       const std::uint32_t ar = ldp<GC>(arec + j);
       const std::uint32_t base = ar & 0xFFFFFFu;
-      if (h.cell_base == 0)  // plan-uniform: entries in the staged acell
-        return base + alias_fast(acell, ar >> 24, base, jj, rare);
+      // acell_s == acell unless the plan has the unstaged tail (then it is in
+      // global memory and ldp<false> is a generic load): branch-free, so the
+      // two groups of a round pair keep independent dependency chains
       return base + alias_fast(acell_s, ar >> 24, base, jj, rare);
     }
   };
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                               (__funnelshift_r(w3, w3, F.y) & 8u);
       return (F.y >> v) & 1u;
     } else {
-      const uint4 F = h.fn_base == 0 ? ldp<GC>(fns + f) : fns_s[f];  // plan-uniform
+      const uint4 F = ldp<GC>(fns_s + f);  // == fns + f unless the plan has the unstaged tail
       std::uint32_t v;
       if constexpr (RG) {
         v = gather4_shfl(wreg, F.z, F.w, 0);
@@ -524,7 +529,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           }
           // two general rounds: both groups' loads before either emit (not in
           // the compact-record variant, whose register budget it would raise)
-          if (!SC && jr0 >= A1) {
+          if (kGeneralPairs && !SC && jr0 >= A1) {
             const std::uint32_t j0 = jr0 + r, j1 = jr1 + r;
             const bool a0 = j0 < A, a1 = j1 < A;
             std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
@@ -718,6 +723,8 @@ kernel_fn pick_place(int place) {
   switch (place) {
     case PLACE_ALL:
       return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, GM>;
+    case PLACE_CORE_PERT:
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE_PERT, GM>;
     case PLACE_TABLES:
       return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, GM>;
     case PLACE_CORE:

@@ -17,15 +17,38 @@ enum { STREAM_U53 = 0, STREAM_U32 = 1 };
 // Plan placement = the staged prefix of the blob (dev_plan.h): 0 nothing (all
 // reads through the read-only L1/L2 path), 1 core, 2 core + tables, 3 also the
 // perturbation cells of the launch's stream.
-enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_TABLES = 2, PLACE_ALL = 3 };
+// PLACE_CORE_PERT (4) stages the core and the launch stream's perturbation
+// cells (two bulk copies; the cells land right after the core) and reads the
+// tables through L1/L2: for plans whose tables are too large but whose cells
+// fit (perturbation-dominated runs, c5 at high p).
+enum { PLACE_GLOBAL = 0, PLACE_CORE = 1, PLACE_TABLES = 2, PLACE_ALL = 3, PLACE_CORE_PERT = 4 };
 
+template <int STREAM>
+__host__ __device__ inline std::uint32_t pert_off(const dev_plan_header& h) {
+  return STREAM == 0 ? h.off_pert53 : h.off_pert32;
+}
+template <int STREAM>
+__host__ __device__ inline std::uint32_t pert_bytes(const dev_plan_header& h) {
+  return STREAM == 0 ? h.blob_bytes - h.off_pert53 : h.off_pert53 - h.off_pert32;
+}
+
+// Shared-memory bytes a launch stages for placement `place`.
 template <int STREAM>
 __host__ __device__ inline std::uint32_t staged_prefix(const dev_plan_header& h, int place) {
   if (place == PLACE_ALL) return STREAM == 0 ? h.blob_bytes : h.off_pert53;
   if (place == PLACE_TABLES) return h.off_pert32;
   if (place == PLACE_CORE) return h.core_bytes;
+  if (place == PLACE_CORE_PERT) return h.core_bytes + pert_bytes<STREAM>(h);
   return 0;
 }
+
+// Which sections a placement reads through L1/L2 instead of shared memory.
+template <int PLACE>
+struct placement {
+  static constexpr bool global_core = PLACE == PLACE_GLOBAL;
+  static constexpr bool global_tables = PLACE != PLACE_TABLES && PLACE != PLACE_ALL;
+  static constexpr bool global_pert = PLACE != PLACE_ALL && PLACE != PLACE_CORE_PERT;
+};
 
 template <bool G, class T>
 __device__ __forceinline__ T ldp(const T* p) {
@@ -39,25 +62,32 @@ __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Stage `bytes` (multiple of 16) from global to shared memory with bulk
-// copies completing on one mbarrier; every thread of the CTA waits.
+// Stage bytes [0, n0) of the blob, then (n1 > 0) n1 bytes from src1 right
+// after them, with bulk copies (multiples of 16 bytes) completing on one
+// mbarrier; every thread of the CTA waits.
 __device__ __forceinline__ void stage_plan(std::uint8_t* dst, const std::uint8_t* src,
-                                           std::uint32_t bytes, std::uint64_t* bar) {
+                                           std::uint32_t n0, std::uint64_t* bar,
+                                           const std::uint8_t* src1 = nullptr,
+                                           std::uint32_t n1 = 0) {
   const std::uint32_t b = smem_u32(bar);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n0 + n1)
                  : "memory");
-    for (std::uint32_t off = 0; off < bytes; off += 32768u) {
-      const std::uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-              "r"(smem_u32(dst + off)),
-          "l"(src + off), "r"(n), "r"(b)
-          : "memory");
-    }
+    auto copy = [&](std::uint8_t* d, const std::uint8_t* sp, std::uint32_t bytes) {
+      for (std::uint32_t off = 0; off < bytes; off += 32768u) {
+        const std::uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(smem_u32(d + off)),
+            "l"(sp + off), "r"(n), "r"(b)
+            : "memory");
+      }
+    };
+    copy(dst, src, n0);
+    if (n1) copy(dst + n0, src1, n1);
   }
   __syncthreads();
   std::uint32_t done = 0;
@@ -69,6 +99,29 @@ __device__ __forceinline__ void stage_plan(std::uint8_t* dst, const std::uint8_t
         : "r"(b)
         : "memory");
   }
+}
+
+// Stage what placement PLACE keeps in shared memory; returns the bytes used.
+template <int STREAM, int PLACE>
+__device__ __forceinline__ std::uint32_t stage_placement(std::uint8_t* smem, const std::uint8_t* gblob,
+                                                         const dev_plan_header& h,
+                                                         std::uint64_t* bar) {
+  const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
+  if constexpr (PLACE == PLACE_CORE_PERT)
+    stage_plan(smem, gblob, h.core_bytes, bar, gblob + pert_off<STREAM>(h), pert_bytes<STREAM>(h));
+  else if (staged)
+    stage_plan(smem, gblob, staged, bar);
+  return staged;
+}
+
+// This stream's perturbation cells for placement PLACE.
+template <int STREAM, int PLACE>
+__device__ __forceinline__ const std::uint8_t* pert_cells(const std::uint8_t* smem,
+                                                          const std::uint8_t* gblob,
+                                                          const dev_plan_header& h) {
+  if constexpr (PLACE == PLACE_CORE_PERT) return smem + h.core_bytes;
+  if constexpr (PLACE == PLACE_ALL) return smem + pert_off<STREAM>(h);
+  return gblob + pert_off<STREAM>(h);
 }
 
 template <int STREAM>

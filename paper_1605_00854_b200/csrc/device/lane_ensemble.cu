@@ -53,19 +53,18 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
                     std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
-  constexpr bool GC = PLACE < PLACE_CORE;
-  constexpr bool GT = PLACE < PLACE_TABLES;
-  constexpr bool GP = PLACE < PLACE_ALL;
+  constexpr bool GC = placement<PLACE>::global_core;    // core sections read from global
+  constexpr bool GT = placement<PLACE>::global_tables;  // tables read from global
+  constexpr bool GP = placement<PLACE>::global_pert;    // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
 
-  const std::uint32_t staged = staged_prefix<STREAM>(h, PLACE);
-  if (staged) stage_plan(smem, gblob, staged, &stage_bar);
+  const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
-  const std::uint8_t* pbase = GP ? gblob : smem;
-  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pbase + h.off_pert53);
-  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pbase + h.off_pert32);
+  const std::uint8_t* pcells = pert_cells<STREAM, PLACE>(smem, gblob, h);
+  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pcells);
+  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pcells);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
@@ -250,16 +249,12 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
           const std::uint32_t ar = ldp<GC>(arec + gi);
           const std::uint32_t base = ar & 0xFFFFFFu, asz = ar >> 24;
           bool rare = exact_all;
-          // plan-uniform branches keep each load in one address space
-          std::uint32_t f = base + (h.cell_base == 0 ? alias_fast(acell, asz, base, r, r32, rare)
-                                                     : alias_fast(acell_s, asz, base, r, r32, rare));
+          // acell_s / fns_s == acell / fns unless the plan has the unstaged
+          // tail of compact plans (global memory; ldp<false> is then generic)
+          std::uint32_t f = base + alias_fast(acell_s, asz, base, r, r32, rare);
           if constexpr (STREAM == STREAM_U53)
             if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r.value());
-          uint4 F;
-          if (h.fn_base == 0)
-            F = ldp<GC>(fns + f);
-          else
-            F = fns_s[f];
+          const uint4 F = ldp<GC>(fns_s + f);
           olo = (F.x >> gather_fn(Sc, F)) & 1u;
           off = gi;
           members = 1;
@@ -369,6 +364,8 @@ lane_kernel_fn pick_lane_place(int place) {
   switch (place) {
     case PLACE_ALL:
       return pbn_lane_kernel<STREAM, PLACE_ALL>;
+    case PLACE_CORE_PERT:
+      return pbn_lane_kernel<STREAM, PLACE_CORE_PERT>;
     case PLACE_TABLES:
       return pbn_lane_kernel<STREAM, PLACE_TABLES>;
     case PLACE_CORE:

@@ -52,7 +52,7 @@ def test_lane_kernel_vs_oracle(pb, orc, cuda_ok, case, stream):
     assert eng.info()["lanes_per_traj"] == 1
 
 
-@pytest.mark.parametrize("placement", ["global", "core", "tables", "all"])
+@pytest.mark.parametrize("placement", ["global", "core", "tables", "all", "core_pert"])
 def test_lane_kernel_placements(pb, orc, cuda_ok, placement):
     plan, pred = _setup(pb, "singles")
     eng = pb.GpuEnsemble(plan, lanes_per_traj=1, placement=placement)

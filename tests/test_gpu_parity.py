@@ -72,7 +72,7 @@ def test_compact_plan_on_fallback_kernels(pb, orc, cuda_ok, lpt):
         assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
 
 
-@pytest.mark.parametrize("placement", ["global", "core", "tables", "all"])
+@pytest.mark.parametrize("placement", ["global", "core", "tables", "all", "core_pert"])
 def test_placement_invariance(pb, orc, cuda_ok, placement):
     plan, pred = _setup(pb, "c2")
     eng = pb.GpuEnsemble(plan, placement=placement)

@@ -7,7 +7,7 @@ o=gpurun_out
 python bench.py > $o/all_default.json 2> $o/all_default.err
 python bench.py --impl reference > $o/all_ref.json 2> $o/all_ref.err
 python bench.py --no-cpu-baseline --stream u32 > $o/all_c2_u32.json 2>> $o/all_default.err
-python bench.py --no-cpu-baseline --config c1 --sim-steps 100000 --steps 3 > $o/all_c1.json 2>> $o/all_default.err
+python bench.py --no-cpu-baseline --config c1 --steps 3 > $o/all_c1.json 2>> $o/all_default.err
 python bench.py --no-cpu-baseline --config c4 --sim-steps 2000 > $o/all_c4.json 2>> $o/all_default.err
 : > $o/all_c5_sweep.jsonl
 for p in 0.1 0.01 0.001 0.0001; do
