@@ -46,7 +46,11 @@ __device__ __noinline__ std::uint32_t alias_exact_fp64(const double* __restrict_
 
 constexpr int kLaneMaxWarps = 28;  // 896 threads: 72 registers per thread
 
-template <int STREAM, int PLACE>
+// SCAN: lanes scan their own steps through phase A up to the next function
+// phase (pays when the function phase is rare, c1); otherwise all lanes take
+// step s together and the function phase runs under divergence (c3, where
+// ~90% of steps reach it).
+template <int STREAM, int PLACE, bool SCAN>
 __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     pbn_lane_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                     const dev_run_params rp, std::uint64_t* __restrict__ states,
@@ -79,6 +83,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t warp = threadIdx.x >> 5;
   const std::uint64_t tloc = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const std::uint32_t lmask = __ballot_sync(0xFFFFFFFFu, tloc < rp.n_traj);  // live lanes
   if (tloc >= rp.n_traj) return;
 
   // per-warp shared memory: two state buffers of sw32 words x 32 lanes, then
@@ -99,6 +104,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   const std::uint32_t k = h.k, g = h.g;
   const bool exact_all = rp.exact_alias != 0;
   const std::uint32_t nb0 = (g + h.has_leaf + DPB - 1) / DPB;  // blocks of phase A
+  const std::uint32_t nplain = g ? (g - 1) / DPB : 0;         // blocks of full-width draws only
   const std::uint32_t A = h.n_alias_groups, NG = h.n_groups, A1 = h.n_single_alias;
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
@@ -180,131 +186,9 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   }
   const std::uint64_t s_end = rp.step_begin + rp.n_steps;
 
-  for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
-    std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
-    const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
-
-    // ---- phase A: draws 0..g (engine.hpp:257-268)
-    bool flip = false, leaf = false;
-    auto phase_a = [&](auto bern_c) {
-      constexpr bool BERN = decltype(bern_c)::value;  // node-wise plans (Method_old / reduction)
-      for (std::uint32_t b = 0; b < nb0; ++b) {
-        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-        const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);
-#pragma unroll
-        for (std::uint32_t e = 0; e < DPB; ++e) {
-          std::uint32_t c;
-          if constexpr (BERN) {
-            if constexpr (STREAM == STREAM_U53)
-              c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
-            else
-              c = pick32(x, e) < h.pthr32 ? 1u : 0u;
-          } else if constexpr (STREAM == STREAM_U53) {
-            c = pert_draw53<GP>(pert53, pick53(x, e), k);
-          } else {
-            c = pert_draw32<GP>(pert32, pick32(x, e), k);
-          }
-          const int q = rem - 1 - static_cast<int>(e);
-          c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
-          if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
-            flip = true;
-            const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
-            Sc[32 * w] ^= c << sh;
-            if (sh != 0 && (c >> (32 - sh)) != 0) Sc[32 * (w + 1)] ^= c >> (32 - sh);
-          }
-          if (q == -1 && h.has_leaf) {
-            if constexpr (STREAM == STREAM_U53)
-              leaf = pick53(x, e).raw() > h.leaf_thr53;
-            else
-              leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
-          }
-        }
-      }
-    };
-    if (h.pert_mode != 0)
-      phase_a(std::true_type{});
-    else
-      phase_a(std::false_type{});
-
-    if (flip) {
-      ++npert;
-    } else if (!leaf) {
-      // ---- function phase: the reference's group loop (engine.hpp:270-311)
-      std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
-      for (std::uint32_t w = 0; w < sw32; ++w) Sn[32 * w] = 0;
-      uint4 xb = make_uint4(0, 0, 0, 0);  // the phase-B block holding draw j
-      for (std::uint32_t gi = 0; gi < NG; ++gi) {
-        raw53 r{0, 0};
-        std::uint32_t r32 = 0;
-        if (gi < A) {  // draw j = gi (alias groups come first)
-          const std::uint32_t e = gi % DPB;
-          if (e == 0) xb = philox_block(sp, nb0 + gi / DPB, rp.rk0, rp.rk1);
-          if constexpr (STREAM == STREAM_U53)
-            r = pick53(xb, e);
-          else
-            r32 = pick32(xb, e);
-        }
-        std::uint32_t olo, ohi = 0, off, members;
-        if (gi < A1) {  // single node at offset gi, inline 1-bit tables (dev_plan.h arec)
-          const std::uint32_t ar = ldp<GC>(arec + gi);
-          const std::uint32_t base = ar & 0xFFFFFFu, asz = ar >> 24;
-          bool rare = exact_all;
-          // acell_s / fns_s == acell / fns unless the plan has the unstaged
-          // tail of compact plans (global memory; ldp<false> is then generic)
-          std::uint32_t f = base + alias_fast(acell_s, asz, base, r, r32, rare);
-          if constexpr (STREAM == STREAM_U53)
-            if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r.value());
-          const uint4 F = ldp<GC>(fns_s + f);
-          olo = (F.x >> gather_fn(Sc, F)) & 1u;
-          off = gi;
-          members = 1;
-        } else {
-          const uint4 G = ldp<GC>(groups + gi);
-          const std::uint32_t asz = G.w & 0x7FFFFFu;
-          members = (G.w >> 24) + 1;
-          off = G.x;
-          std::uint32_t idx = 0;
-          if (asz != 0) {
-            bool rare = exact_all || (G.w & kGroupExactAlias);
-            idx = alias_fast(acell, asz, G.z, r, r32, rare);
-            if constexpr (STREAM == STREAM_U53)
-              if (__builtin_expect(rare, 0)) idx = alias_exact_fp64(acut, aidx, asz, G.z + h.cell_base, r.value());
-          }
-          const uint4 F = ldp<GC>(fns + G.y + idx);
-          const std::uint32_t v = gather_fn(Sc, F);
-          if (F.y & 0x80u) {  // inline table
-            const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
-            olo = (F.x >> (v * members)) & m;
-          } else {
-            const std::uint32_t el2 = (F.y >> 5) & 3u;
-            if (el2 == 0) {
-              olo = ldp<GT>(tab + F.x + v);
-            } else if (el2 == 1) {
-              olo = ldp<GT>(reinterpret_cast<const std::uint16_t*>(tab + F.x) + v);
-            } else if (el2 == 2) {
-              olo = ldp<GT>(reinterpret_cast<const std::uint32_t*>(tab + F.x) + v);
-            } else {
-              const uint2 o = ldp<GT>(reinterpret_cast<const uint2*>(tab + F.x) + v);
-              olo = o.x;
-              ohi = o.y;
-            }
-          }
-        }
-        // next |= out << offset (engine.hpp:304-309); offset and width are
-        // the group's, so the branches are warp-uniform
-        const std::uint32_t w = off >> 5, sh = off & 31;
-        Sn[32 * w] |= olo << sh;
-        if (sh + members > 32) {
-          Sn[32 * (w + 1)] |= sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
-          if (sh + members > 64) Sn[32 * (w + 2)] |= ohi >> (32 - sh);
-        }
-      }
-      cur ^= 1;
-      Sc = Sn;
-      ++nfn;
-    }
-
-    // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
+  // Statistics of step s on the state after it (engine.hpp:375-381) +
+  // sampled predicate transitions, series bits and node counts.
+  auto step_stats = [&](const std::uint32_t* Sc, std::uint64_t s) {
     const std::uint32_t hit = pred_eval(Sc);
     nhit += hit;
     if (++kphase == rp.kappa) {
@@ -336,6 +220,184 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
         sword = 0;
       }
     }
+  };
+
+  // Phase A of step `sp` on state Sc (engine.hpp:257-268): flips XORed in.
+  auto phase_a_step = [&](std::uint32_t* Sc, const step_philox& sp, bool& flip, bool& leaf) {
+    flip = false;
+    leaf = false;
+    // blocks [0, nplain) hold full-width pattern draws only (no per-draw
+    // mask or leaf test); the tail blocks hold the last group and the leaf draw
+    auto phase_a = [&](auto bern_c) {
+      constexpr bool BERN = decltype(bern_c)::value;  // node-wise plans (Method_old / reduction)
+      auto elem = [&](const uint4& x, std::uint32_t b, std::uint32_t e, bool tail) {
+        std::uint32_t c;
+        if constexpr (BERN) {
+          if constexpr (STREAM == STREAM_U53)
+            c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
+          else
+            c = pick32(x, e) < h.pthr32 ? 1u : 0u;
+        } else if constexpr (STREAM == STREAM_U53) {
+          c = pert_draw53<GP>(pert53, pick53(x, e), k);
+        } else {
+          c = pert_draw32<GP>(pert32, pick32(x, e), k);
+        }
+        const int q = static_cast<int>(g) - 1 - static_cast<int>(b * DPB + e);
+        if (tail) c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+        if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+          flip = true;
+          const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
+          Sc[32 * w] ^= c << sh;
+          if (sh != 0 && (c >> (32 - sh)) != 0) Sc[32 * (w + 1)] ^= c >> (32 - sh);
+        }
+        if (tail && q == -1 && h.has_leaf) {  // the leaf draw (engine.hpp:268)
+          if constexpr (STREAM == STREAM_U53)
+            leaf = pick53(x, e).raw() > h.leaf_thr53;
+          else
+            leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
+        }
+      };
+      for (std::uint32_t b = 0; b < nplain; ++b) {
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, false);
+      }
+      for (std::uint32_t b = nplain; b < nb0; ++b) {
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, true);
+      }
+    };
+    if (h.pert_mode != 0)
+      phase_a(std::true_type{});
+    else
+      phase_a(std::false_type{});
+
+  };
+
+  // Function phase of step `sp` (engine.hpp:270-311): the reference's group
+  // loop from state Sc into Sn.
+  auto fn_phase = [&](const std::uint32_t* Sc, std::uint32_t* Sn, const step_philox& sp) {
+    for (std::uint32_t w = 0; w < sw32; ++w) Sn[32 * w] = 0;
+    uint4 xb = make_uint4(0, 0, 0, 0);  // the phase-B block holding draw j
+    for (std::uint32_t gi = 0; gi < NG; ++gi) {
+      raw53 r{0, 0};
+      std::uint32_t r32 = 0;
+      if (gi < A) {  // draw j = gi (alias groups come first)
+        const std::uint32_t e = gi % DPB;
+        if (e == 0) xb = philox_block(sp, nb0 + gi / DPB, rp.rk0, rp.rk1);
+        if constexpr (STREAM == STREAM_U53)
+          r = pick53(xb, e);
+        else
+          r32 = pick32(xb, e);
+      }
+      std::uint32_t olo, ohi = 0, off, members;
+      if (gi < A1) {  // single node at offset gi, inline 1-bit tables (dev_plan.h arec)
+        const std::uint32_t ar = ldp<GC>(arec + gi);
+        const std::uint32_t base = ar & 0xFFFFFFu, asz = ar >> 24;
+        bool rare = exact_all;
+        // acell_s / fns_s == acell / fns unless the plan has the unstaged
+        // tail of compact plans (global memory; ldp<false> is then generic)
+        std::uint32_t f = base + alias_fast(acell_s, asz, base, r, r32, rare);
+        if constexpr (STREAM == STREAM_U53)
+          if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r.value());
+        const uint4 F = ldp<GC>(fns_s + f);
+        olo = (F.x >> gather_fn(Sc, F)) & 1u;
+        off = gi;
+        members = 1;
+      } else {
+        const uint4 G = ldp<GC>(groups + gi);
+        const std::uint32_t asz = G.w & 0x7FFFFFu;
+        members = (G.w >> 24) + 1;
+        off = G.x;
+        std::uint32_t idx = 0;
+        if (asz != 0) {
+          bool rare = exact_all || (G.w & kGroupExactAlias);
+          idx = alias_fast(acell, asz, G.z, r, r32, rare);
+          if constexpr (STREAM == STREAM_U53)
+            if (__builtin_expect(rare, 0)) idx = alias_exact_fp64(acut, aidx, asz, G.z + h.cell_base, r.value());
+        }
+        const uint4 F = ldp<GC>(fns + G.y + idx);
+        const std::uint32_t v = gather_fn(Sc, F);
+        if (F.y & 0x80u) {  // inline table
+          const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
+          olo = (F.x >> (v * members)) & m;
+        } else {
+          const std::uint32_t el2 = (F.y >> 5) & 3u;
+          if (el2 == 0) {
+            olo = ldp<GT>(tab + F.x + v);
+          } else if (el2 == 1) {
+            olo = ldp<GT>(reinterpret_cast<const std::uint16_t*>(tab + F.x) + v);
+          } else if (el2 == 2) {
+            olo = ldp<GT>(reinterpret_cast<const std::uint32_t*>(tab + F.x) + v);
+          } else {
+            const uint2 o = ldp<GT>(reinterpret_cast<const uint2*>(tab + F.x) + v);
+            olo = o.x;
+            ohi = o.y;
+          }
+        }
+      }
+      // next |= out << offset (engine.hpp:304-309); offset and width are
+      // the group's, so the branches are warp-uniform
+      const std::uint32_t w = off >> 5, sh = off & 31;
+      Sn[32 * w] |= olo << sh;
+      if (sh + members > 32) {
+        Sn[32 * (w + 1)] |= sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
+        if (sh + members > 64) Sn[32 * (w + 2)] |= ohi >> (32 - sh);
+      }
+    }
+  };
+
+  if constexpr (SCAN) {
+    // The class of a step (perturbed / leaf no-op / function phase) depends
+    // on the stream only, never on the state: each lane scans its own steps
+    // through phase A until one needs the function phase, so the warp runs
+    // the (expensive, per-lane) function phase with every lane that still has
+    // steps, instead of with the ~(1-p)^n' share whose current step needs it.
+    std::uint64_t s = rp.step_begin;
+    for (;;) {
+      bool need = false;
+      step_philox sp{};
+      while (s < s_end) {
+        sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+        bool flip, leaf;
+        std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
+        phase_a_step(Sc, sp, flip, leaf);
+        if (!flip && !leaf) {
+          need = true;
+          break;
+        }
+        npert += flip ? 1u : 0u;
+        step_stats(Sc, s);
+        ++s;
+      }
+      if (!__any_sync(lmask, need)) break;
+      if (need) {
+        std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
+        fn_phase(wbuf + cur * (sw32 * 32), Sn, sp);
+        cur ^= 1;
+        ++nfn;
+        step_stats(Sn, s);
+        ++s;
+      }
+    }
+  } else {
+    for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
+      std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
+      const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+      bool flip, leaf;
+      phase_a_step(Sc, sp, flip, leaf);
+      if (flip) {
+        ++npert;
+      } else if (!leaf) {
+        std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
+        fn_phase(Sc, Sn, sp);
+        cur ^= 1;
+        Sc = Sn;
+        ++nfn;
+      }
+      step_stats(Sc, s);
+    }
   }
   if (rp.node_counts && nc_pending) nc_flush();
   if (rp.tprev) rp.tprev[tloc] = static_cast<std::uint8_t>(prev | (kphase << 2));
@@ -359,19 +421,19 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
 using lane_kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
                                 std::uint64_t*, std::uint64_t*);
 
-template <int STREAM>
+template <int STREAM, bool SCAN>
 lane_kernel_fn pick_lane_place(int place) {
   switch (place) {
     case PLACE_ALL:
-      return pbn_lane_kernel<STREAM, PLACE_ALL>;
+      return pbn_lane_kernel<STREAM, PLACE_ALL, SCAN>;
     case PLACE_CORE_PERT:
-      return pbn_lane_kernel<STREAM, PLACE_CORE_PERT>;
+      return pbn_lane_kernel<STREAM, PLACE_CORE_PERT, SCAN>;
     case PLACE_TABLES:
-      return pbn_lane_kernel<STREAM, PLACE_TABLES>;
+      return pbn_lane_kernel<STREAM, PLACE_TABLES, SCAN>;
     case PLACE_CORE:
-      return pbn_lane_kernel<STREAM, PLACE_CORE>;
+      return pbn_lane_kernel<STREAM, PLACE_CORE, SCAN>;
     default:
-      return pbn_lane_kernel<STREAM, PLACE_GLOBAL>;
+      return pbn_lane_kernel<STREAM, PLACE_GLOBAL, SCAN>;
   }
 }
 
@@ -387,12 +449,14 @@ std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts) {
 }
 
 cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
-                                 int stream_kind, std::uint32_t warps_per_cta,
+                                 int stream_kind, bool scan, std::uint32_t warps_per_cta,
                                  const dev_run_params& rp, std::uint64_t* d_states,
                                  std::uint64_t* d_counts, cudaStream_t stream,
                                  std::uint32_t* launches) {
-  const lane_kernel_fn fn = stream_kind == STREAM_U53 ? pick_lane_place<STREAM_U53>(place)
-                                                      : pick_lane_place<STREAM_U32>(place);
+  const lane_kernel_fn fn =
+      stream_kind == STREAM_U53
+          ? (scan ? pick_lane_place<STREAM_U53, true>(place) : pick_lane_place<STREAM_U53, false>(place))
+          : (scan ? pick_lane_place<STREAM_U32, true>(place) : pick_lane_place<STREAM_U32, false>(place));
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t grid = (rp.n_traj + threads - 1) / threads;
   const std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
