@@ -33,13 +33,19 @@ namespace pbn_b200 {
 #define PBN_GENERAL_PAIRS 1
 #endif
 constexpr bool kGeneralPairs = PBN_GENERAL_PAIRS != 0;
+#ifndef PBN_RG2
+#define PBN_RG2 1
+#endif
+constexpr bool kUseRg2 = PBN_RG2 != 0;
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
 constexpr int kMaxWarpsLpt32 = 28;
 
 // GM: parent gather mode — 0 shared-memory state words, 1 one state word per
-// lane with shuffles (RG), 2 RG with the compact single-node records (SC).
+// lane with shuffles (RG), 2 RG with the compact single-node records (SC), 3
+// two state words per lane (RG2, n' <= 2047) for the single-node groups
+// (general groups gather from shared memory: they run under divergence).
 template <int LPT, int STREAM, int PLACE, int GM>
 __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
@@ -52,6 +58,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool GP = placement<PLACE>::global_pert;    // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
   constexpr bool RG = GM >= 1;
+  constexpr bool RG2 = GM == 3;
   constexpr bool SC = GM == 2;
 
   const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     else
       return base + pick;
   };
+  std::uint32_t wreg1 = 0;  // RG2: state word `lane + 32` of the current state
   auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
     if constexpr (SC) {
       // compact record: 10-bit records (word << 5 | rotation), table at bits 16..31
@@ -335,7 +343,14 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     } else {
       const uint4 F = ldp<GC>(fns_s + f);  // == fns + f unless the plan has the unstaged tail
       std::uint32_t v;
-      if constexpr (RG) {
+      if constexpr (RG2) {
+        v = gather4_shfl2(wreg, wreg1, F.z, F.w, 0);
+        if (h.single_gc5) {  // plan-uniform
+          uint2 rr = make_uint2(zrec01, zrec23);
+          if ((F.y & 31u) > 4) rr = ldp<GC>(grec + (F.y >> 8));
+          v |= gather4_shfl2(wreg, wreg1, rr.x, rr.y, 4);
+        }
+      } else if constexpr (RG) {
         v = gather4_shfl(wreg, F.z, F.w, 0);
         if (h.single_gc5) {  // plan-uniform: every lane takes the same branch
           uint2 rr = make_uint2(zrec01, zrec23);
@@ -457,6 +472,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
       std::uint32_t wreg = 0;  // RG: state word `lane` of the current state
       if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
+      if constexpr (RG2) wreg1 = lane + 32 < sw32 ? Sc[lane + 32] : 0u;
       // alias region: chunks of LPT*DPB draws; lane r first computes phase-B
       // block nb0 + j0/DPB + r into the draw buffer
       // lane r computes blocks q*LPT + r of each chunk (independent chains)
@@ -748,7 +764,8 @@ kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
     case 16:
       return pick_place<16, STREAM, 0>(place);
     default:
-      return gm == 2   ? pick_place<32, STREAM, 2>(place)
+      return gm == 3   ? pick_place<32, STREAM, 3>(place)
+             : gm == 2 ? pick_place<32, STREAM, 2>(place)
              : gm == 1 ? pick_place<32, STREAM, 1>(place)
                        : pick_place<32, STREAM, 0>(place);
   }
@@ -769,7 +786,8 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches) {
   const bool rg = lpt == 32 && h.rg_ok && h.n_single_alias >= 32;
-  const int gm = !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
+  const bool rg2 = lpt == 32 && !h.rg_ok && h.sw32 <= 64 && h.n_single_alias >= 32 && kUseRg2;
+  const int gm = rg2 ? 3 : !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
   const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm);
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;

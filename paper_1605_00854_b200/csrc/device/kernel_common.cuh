@@ -182,6 +182,24 @@ __device__ __forceinline__ std::uint32_t gather4(const std::uint32_t* S, std::ui
          (__funnelshift_r(w2, w2, r2) & (4u << b0)) | (__funnelshift_r(w3, w3, r3) & (8u << b0));
 }
 
+// Same, with two state words per lane (1023 < n' <= 2047: word w lives in
+// lane w & 31, register w >> 5): both registers are shuffled and bit 10 of
+// the record (bit 5 of the word index) picks one.
+__device__ __forceinline__ std::uint32_t gather4_shfl2(std::uint32_t wr0, std::uint32_t wr1,
+                                                       std::uint32_t p01, std::uint32_t p23,
+                                                       std::uint32_t b0) {
+  auto get = [&](std::uint32_t rec) {
+    const std::uint32_t a = __shfl_sync(0xFFFFFFFFu, wr0, rec >> 5);
+    const std::uint32_t b = __shfl_sync(0xFFFFFFFFu, wr1, rec >> 5);
+    return (rec & 0x400u) ? b : a;
+  };
+  const std::uint32_t w0 = get(p01), w1 = get(p01 >> 16), w2 = get(p23), w3 = get(p23 >> 16);
+  return (__funnelshift_r(w0, w0, p01) & (1u << b0)) |
+         (__funnelshift_r(w1, w1, p01 >> 16) & (2u << b0)) |
+         (__funnelshift_r(w2, w2, p23) & (4u << b0)) |
+         (__funnelshift_r(w3, w3, p23 >> 16) & (8u << b0));
+}
+
 // Same, with the state held in a lane's column of a [word][32 lanes] array
 // (lane_ensemble.cu): word w of the lane's trajectory at col[32 * w], so
 // record r's word is col[r & ~31] and 32 lanes hit 32 distinct banks.
