@@ -491,6 +491,16 @@ def run_ours(a):
     peak_lookups = props.multi_processor_count * 32 * sm_mhz * 1e6
     lookups = flat.expected_lookups(fn_total, traj_steps)
     achieved = lookups / (total_ms / 1e3) / world
+    # Ceiling the injected stream imposes: a kernel issuing
+    # nothing but the Philox4x32-10 blocks of the workload (>= 36 lane-
+    # instructions per block) at the SMs' issue peak (4 warp-instr/clk/SM).
+    dpb = 2 if stream == pb.STREAM_U53 else 4
+    n_alias = int(np.count_nonzero(flat.grp_alias_size))
+    has_leaf = 1 if a.method != "old" else 0
+    blocks = (-(-(flat.pert_groups + has_leaf) // dpb)) * traj_steps + (-(-n_alias // dpb)) * fn_total
+    issue_peak = props.multi_processor_count * 4 * sm_mhz * 1e6
+    rng_ceiling_steps = issue_peak / (blocks * 36 / 32 / traj_steps)
+    rng_ceiling = rng_ceiling_steps * lookups / traj_steps
     info = eng.info()
     spill = None
     if info["placement"] == "global":
@@ -526,12 +536,17 @@ def run_ours(a):
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                      "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-                     "issue_bound_evidence": "profiles/r01_c2_k16_u53_v4.txt: issue slots ~71% "
-                                             "busy, ALU pipe ~67%, smem wavefronts ~68%",
+                     "issue_bound_evidence": "profiles/r01_c2_k16_u53_v6.txt: issue slots ~71% "
+                                             "busy, ALU pipe ~68%, smem wavefronts ~48% of peak",
                      "note": "lookup roofline = SMs x 32 probes/clk x sm_max_mhz "
                              "(MEASURED_PEAKS.json); algorithmic lookups = g per step + "
                              "(A+G) per function-phase step (SURVEY 8d), per GPU",
-                     "lookups_per_step": lookups / traj_steps},
+                     "lookups_per_step": lookups / traj_steps,
+                     "rng_ceiling_frac": rng_ceiling / peak_lookups,
+                     "frac_of_rng_ceiling": achieved / rng_ceiling,
+                     "rng_ceiling_note": "lookup rate of a kernel issuing only the workload's "
+                                         "Philox4x32-10 blocks (36 lane-instr each) at the issue "
+                                         "peak; DESIGN.md section 7"},
         "clocks": clk.summary(),
     }
     if not a.no_cpu_baseline and world == 1:

@@ -31,6 +31,8 @@ def test_bench_line_has_contract_keys():
     assert d["gpu_launches"] == 2
     r = d["roofline"]
     assert 0 < r["frac"] < 1 and r["peak"] > 0 and abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+    # the stream's own ceiling sits below the lookup peak
+    assert 0 < r["rng_ceiling_frac"] < 1 and 0 < r["frac_of_rng_ceiling"] < 1
     assert d["config"]["workload"].startswith("c2")
 
 
