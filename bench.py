@@ -424,9 +424,9 @@ def run_ours(a):
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)  # measurement: max over ranks
     total_ms = float(t_ms.item())
     # the single collective of the path: one all-reduce of the pooled counts
-    local = pooled(counts.cpu().numpy().view(np.uint64))
-    local[6] = fn_steps  # function-phase steps over all timed launches
-    totals = allreduce_totals(local, device=dev)
+    mine = pooled(counts.cpu().numpy().view(np.uint64))
+    mine[6] = fn_steps  # function-phase steps over all timed launches
+    totals = allreduce_totals(mine, device=dev)
     fn_total = int(totals[6])
     traj_steps = n_traj * world * sim_steps * a.steps
     value = traj_steps * flat.n_kept / (total_ms / 1e3)
