@@ -72,6 +72,7 @@ struct pbn_gpu {
   std::uint32_t lpt_fixed = 0;  // 0: chosen per run
   std::uint32_t last_lpt = 0;
   double p_fn = 1.0;  // probability that a step reaches the function phase
+  double p_group_flip = 0.0;  // probability that a full perturbation group flips
 };
 
 namespace {
@@ -113,10 +114,22 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // Lane kernel: scan phase A ahead per lane when fewer steps than this reach
 // the function phase (c1: 0.37 -> +22%; c3: 0.91 -> -17%).
 constexpr double kScanBelow = 0.65;
+// Word-per-block phase A above this per-group flip probability.
+constexpr double kWordsAbove = 0.05;
 
 // Probability that a step reaches the function phase: no kept node flips
 // (every pattern draw returns 0, or every Bernoulli draw misses) and the leaf
 // draw stays below t (engine.hpp:259-268). Exact for the plan's own cells.
+// Probability that a full perturbation group draws a non-zero pattern.
+double group_flip_probability(const pbn_plan_view& v) {
+  if (v.pert_mode != 0 || v.pert_size == 0) return v.pert_mode != 0 ? v.pert_p : 0.0;
+  double zero = 0;
+  const double n = static_cast<double>(v.pert_size);
+  for (std::uint32_t c = 0; c < v.pert_size; ++c)
+    zero += (c == 0 ? v.pert_cut[c] / n : 0.0) + (v.pert_alias[c] == 0 ? (1.0 - v.pert_cut[c]) / n : 0.0);
+  return 1.0 - zero;
+}
+
 double fn_phase_probability(const pbn_plan_view& v) {
   double p_none;
   if (v.pert_mode != 0) {
@@ -239,6 +252,14 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
   const bool nc = (a.flags & PBN_RUN_NODE_COUNTS) != 0;
   if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
   rp.node_counts = nc ? d_node_counts : nullptr;
+  // word-per-block phase A (U53): pays when groups flip often or a lane owns
+  // several phase-A blocks (c5: +2..11 % over p = 1e-4..0.1); with one block
+  // per lane and rare flips (c2) the per-draw path is ~1 % faster
+  {
+    const std::uint32_t lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
+    const std::uint32_t blocks53 = (g.ep.h.g + g.ep.h.has_leaf + 1) / 2;
+    rp.phase_a_words = (g.p_group_flip > kWordsAbove || blocks53 > lpt) ? 1u : 0u;
+  }
   ck(cudaSetDevice(g.device), "cudaSetDevice");
   g.last_lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
   // the counter planes take shared memory: fall back to a leaner plan
@@ -506,6 +527,7 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
     g->lpt_fixed = lpt;
     g->ep = encode_plan(*view);
     g->p_fn = fn_phase_probability(*view);
+    g->p_group_flip = group_flip_probability(*view);
     ck(cudaSetDevice(device), "cudaSetDevice");
     int optin = 0, sms = 0;
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");

@@ -456,8 +456,48 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t b = r; b < nb0; b += LPT) phase_a_block(b, bern_c);
       }
     };
+    // k * DPB == 32 (U53 with k = 16, U32 with k = 8): block b's patterns
+    // fill exactly state word b, which no other lane touches — the patterns
+    // are OR-ed into one word and XOR-ed in with a plain read-modify-write
+    // instead of per-draw atomics (c5 at p = 0.1 flips ~3 groups per lane and
+    // step). Masks only matter in the block of the last group / leaf draw.
+    auto phase_a_words = [&]() {
+      if constexpr (STREAM != STREAM_U53) return;  // U53 only (U32 kernels keep their code)
+      constexpr std::uint32_t K = 32 / DPB;
+      for (std::uint32_t b = r; b < nb0; b += LPT) {
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+        const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
+        std::uint32_t wd = 0;
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) {
+          std::uint32_t c;
+          if constexpr (STREAM == STREAM_U53)
+            c = pert_draw53<GP>(pert53, pick53(x, e), K);
+          else
+            c = pert_draw32<GP>(pert32, pick32(x, e), K);
+          const int q = rem - 1 - static_cast<int>(e);
+          c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+          wd |= c << (e * K);
+        }
+        if (rem <= static_cast<int>(DPB) && h.has_leaf) {  // the leaf draw is element rem
+          const std::uint32_t el = static_cast<std::uint32_t>(rem);
+          if (el < DPB) {
+            if constexpr (STREAM == STREAM_U53)
+              leaf = pick53(x, el).raw() > h.leaf_thr53;
+            else
+              leaf = !h.leaf_never && pick32(x, el) > h.leaf_thr32;
+          }
+        }
+        if (__builtin_expect(wd != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58), word b alone
+          flip = true;
+          Sc[b] ^= wd;
+        }
+      }
+    };
     if (h.pert_mode != 0)  // plan-uniform
       phase_a(std::true_type{});
+    else if (STREAM == STREAM_U53 && rp.phase_a_words && h.k * DPB == 32)
+      phase_a_words();
     else
       phase_a(std::false_type{});
     const bool any_flip = __ballot_sync(smask, flip) != 0;
