@@ -150,11 +150,11 @@ double fn_phase_probability(const pbn_plan_view& v) {
 // Lanes per trajectory: by network size, then doubled until the ensemble
 // gives ~24 resident warps per SM (latency hiding) or one warp per trajectory.
 // Lane-per-trajectory kernel (lane_ensemble.cu) for networks up to 255 kept
-// nodes once the ensemble gives >= 10 warps of 32 trajectories per SM
-// (measured on c1/c3: 2.1-2.2x over sub-warps at 131072 trajectories, behind
-// them below ~40000).
+// nodes once the ensemble gives >= 6 warps of 32 trajectories per SM
+// (measured on c1/c3: +10-30 % over sub-warps at 32768 trajectories, 2-3x at
+// 131072; behind them at 16384).
 std::uint32_t auto_lpt(std::uint32_t n_kept, std::uint64_t n_traj, std::uint32_t sms) {
-  if (n_kept <= 255 && n_traj >= static_cast<std::uint64_t>(sms) * 320) return 1;
+  if (n_kept <= 255 && n_traj >= static_cast<std::uint64_t>(sms) * 192) return 1;
   std::uint32_t lpt = n_kept <= 256 ? 8 : n_kept <= 512 ? 16 : 32;
   while (lpt < 32 && n_traj * lpt / 32 < static_cast<std::uint64_t>(sms) * 24) lpt *= 2;
   return lpt;

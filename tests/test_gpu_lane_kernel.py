@@ -149,10 +149,10 @@ def test_lane_kernel_nodewise_plans(pb, orc, cuda_ok, reduction):
 
 def test_auto_selection_large_ensemble(pb, orc, cuda_ok):
     """lanes_per_traj=0 picks the lane kernel for a small network once the
-    ensemble reaches ~10 warps of trajectories per SM."""
+    ensemble reaches ~6 warps of trajectories per SM."""
     plan, pred = _setup(pb, "c3")
     eng = pb.GpuEnsemble(plan)
-    n = 148 * 320 + 7
+    n = 148 * 192 + 7
     st, cnt = eng.simulate(seed=6, n_traj=n, n_steps=40, pred=pred)
     assert eng.info()["lanes_per_traj"] == 1
     ost, ocnt = orc.simulate(plan.view, 6, 0, n, 40, pred=pred)
