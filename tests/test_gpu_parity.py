@@ -20,6 +20,8 @@ CASES = {
     "tiny": (6, (1, 3), (1, 3), 0.25, 0.0, 2, False, 7, 3, 18),
     # n' <= 1023 with 5-parent functions: exercises the register/shuffle gather's 5th slot
     "p5": (900, (1, 4), (1, 5), 0.002, 0.0, 2, False, 11, 12, 8),
+    # k=16 with two phase-A blocks per lane and frequent flips: the word-per-block phase A
+    "c5_k16": (2000, (1, 3), (1, 4), 0.1, 0.0, 2, False, 1609, 16, 8),
     # 1023 < n' <= 2047 with 5-parent functions: two state words per lane (RG2)
     "p5w": (1500, (1, 3), (1, 5), 0.001, 0.0, 2, False, 12, 12, 8),
     "c4": (5000, (1, 4), (1, 5), 0.0001, 0.0, 2, False, 1608, 12, 12),
@@ -38,7 +40,7 @@ def cuda_ok(pb):
     assert pb.device_count() >= 1, "no CUDA device visible"
 
 
-@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16", "p5", "p5w", "c4"])
+@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16", "c5_k16", "p5", "p5w", "c4"])
 @pytest.mark.parametrize("stream", [0, 1])
 def test_bit_exact_vs_oracle(pb, orc, cuda_ok, case, stream):
     plan, pred = _setup(pb, case)
