@@ -37,6 +37,10 @@ constexpr bool kGeneralPairs = PBN_GENERAL_PAIRS != 0;
 #define PBN_RG2 1
 #endif
 constexpr bool kUseRg2 = PBN_RG2 != 0;
+#ifndef PBN_PLAIN_SHFL
+#define PBN_PLAIN_SHFL 1
+#endif
+constexpr bool kPlainShfl = PBN_PLAIN_SHFL != 0;
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
@@ -220,9 +224,29 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // One group of the function phase (engine.hpp:281-310): combined-function
   // choice, gather of its own parents, table lookup. Returns the packed member
   // outputs; `off`/`members` describe where they go.
+  // UNI (RG kernels): every lane of the warp evaluates a group (the plain
+  // region's rounds, inactive lanes on a clamped index), so the parents can
+  // come by shuffles; the extra-record loop runs to the warp's widest gather.
+  std::uint32_t wreg_s = 0;  // RG: state word `lane` of the current state (set per function phase)
+  std::uint32_t wreg1 = 0;   // RG2: state word `lane + 32`
+  auto gather_fn_shfl = [&](const uint4& F) -> std::uint32_t {
+    const std::uint32_t gc = F.y & 31u;
+    std::uint32_t v = RG2 ? gather4_shfl2(wreg_s, wreg1, F.z, F.w, 0) : gather4_shfl(wreg_s, F.z, F.w, 0);
+    const std::uint32_t gmax = __reduce_max_sync(smask, gc);
+    const std::uint32_t xq = F.y >> 8;
+    for (std::uint32_t q = 4; q < gmax; q += 4) {
+      const bool has = q < gc;
+      const uint2 rr = has ? ldp<GC>(grec + xq + ((q - 4) >> 2)) : make_uint2(F.z, F.w);
+      const std::uint32_t t =
+          RG2 ? gather4_shfl2(wreg_s, wreg1, rr.x, rr.y, q) : gather4_shfl(wreg_s, rr.x, rr.y, q);
+      if (has) v |= t;
+    }
+    return v;
+  };
   auto eval_group = [&](const std::uint32_t* Sc, std::uint32_t gi, std::uint32_t jj,
                         std::uint32_t& olo, std::uint32_t& ohi, std::uint32_t& off,
-                        std::uint32_t& members) {
+                        std::uint32_t& members, auto uni_c) {
+    constexpr bool UNI = decltype(uni_c)::value && RG && LPT == 32;
     const uint4 G = ldp<GC>(groups + gi);
     const std::uint32_t asz = G.w & 0x7FFFFFu;
     members = (G.w >> 24) + 1;
@@ -230,7 +254,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     const std::uint32_t idx =
         asz != 0 ? alias_pick(asz, G.z, jj, exact_all || (G.w & kGroupExactAlias)) : 0u;
     const uint4 F = ldp<GC>(fns + G.y + idx);
-    const std::uint32_t v = gather_fn(Sc, F);
+    std::uint32_t v;
+    if constexpr (UNI)
+      v = gather_fn_shfl(F);
+    else
+      v = gather_fn(Sc, F);
     ohi = 0;
     if (F.y & 0x80u) {  // inline table
       const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
@@ -326,7 +354,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     else
       return base + pick;
   };
-  std::uint32_t wreg1 = 0;  // RG2: state word `lane + 32` of the current state
   auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
     if constexpr (SC) {
       // compact record: 10-bit records (word << 5 | rotation), table at bits 16..31
@@ -512,6 +539,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
       std::uint32_t wreg = 0;  // RG: state word `lane` of the current state
       if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
+      wreg_s = wreg;
       if constexpr (RG2) wreg1 = lane + 32 < sw32 ? Sc[lane + 32] : 0u;
       // alias region: chunks of LPT*DPB draws; lane r first computes phase-B
       // block nb0 + j0/DPB + r into the draw buffer
@@ -589,8 +617,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             const std::uint32_t j0 = jr0 + r, j1 = jr1 + r;
             const bool a0 = j0 < A, a1 = j1 < A;
             std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
-            if (a0) eval_group(Sc, j0, t * LPT + r, lo0, hi0, off0, m0);
-            if (a1) eval_group(Sc, j1, (t + 1) * LPT + r, lo1, hi1, off1, m1);
+            if (a0) eval_group(Sc, j0, t * LPT + r, lo0, hi0, off0, m0, std::false_type{});
+            if (a1) eval_group(Sc, j1, (t + 1) * LPT + r, lo1, hi1, off1, m1, std::false_type{});
             emit_round(Sn, a0, lo0, hi0, off0, m0);
             if (jr1 < A) emit_round(Sn, a1, lo1, hi1, off1, m1);
             continue;
@@ -611,7 +639,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             } else {
               const bool act = j < A;
               std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
-              if (act) eval_group(Sc, j, (t + u) * LPT + r, olo, ohi, off, members);
+              if (act) eval_group(Sc, j, (t + u) * LPT + r, olo, ohi, off, members, std::false_type{});
               emit_round(Sn, act, olo, ohi, off, members);
             }
           }
@@ -624,8 +652,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         const std::uint32_t g0 = gr + r, g1 = gr + LPT + r;
         const bool a0 = g0 < NG, a1 = g1 < NG;
         std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
-        if (a0) eval_group(Sc, g0, 0, lo0, hi0, off0, m0);
-        if (a1) eval_group(Sc, g1, 0, lo1, hi1, off1, m1);
+        if constexpr (RG && LPT == 32 && kPlainShfl) {  // every lane evaluates (clamped), shuffles
+          eval_group(Sc, a0 ? g0 : NG - 1, 0, lo0, hi0, off0, m0, std::true_type{});
+          eval_group(Sc, a1 ? g1 : NG - 1, 0, lo1, hi1, off1, m1, std::true_type{});
+        } else {
+          if (a0) eval_group(Sc, g0, 0, lo0, hi0, off0, m0, std::false_type{});
+          if (a1) eval_group(Sc, g1, 0, lo1, hi1, off1, m1, std::false_type{});
+        }
         emit_round(Sn, a0, lo0, hi0, off0, m0);
         if (gr + LPT < NG) emit_round(Sn, a1, lo1, hi1, off1, m1);
       }
