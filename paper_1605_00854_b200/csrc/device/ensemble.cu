@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   auto eval_group = [&](const std::uint32_t* Sc, std::uint32_t gi, std::uint32_t jj,
                         std::uint32_t& olo, std::uint32_t& ohi, std::uint32_t& off,
                         std::uint32_t& members, auto uni_c) {
-    constexpr bool UNI = decltype(uni_c)::value && RG && LPT == 32;
+    constexpr bool UNI = decltype(uni_c)::value && RG && !RG2 && LPT == 32;
     const uint4 G = ldp<GC>(groups + gi);
     const std::uint32_t asz = G.w & 0x7FFFFFu;
     members = (G.w >> 24) + 1;
@@ -617,8 +617,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             const std::uint32_t j0 = jr0 + r, j1 = jr1 + r;
             const bool a0 = j0 < A, a1 = j1 < A;
             std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
-            if (a0) eval_group(Sc, j0, t * LPT + r, lo0, hi0, off0, m0, std::false_type{});
-            if (a1) eval_group(Sc, j1, (t + 1) * LPT + r, lo1, hi1, off1, m1, std::false_type{});
+            if constexpr (RG && !RG2 && LPT == 32 && kPlainShfl) {  // uniform, shuffle gathers
+              eval_group(Sc, a0 ? j0 : A - 1, t * LPT + r, lo0, hi0, off0, m0, std::true_type{});
+              eval_group(Sc, a1 ? j1 : A - 1, (t + 1) * LPT + r, lo1, hi1, off1, m1, std::true_type{});
+            } else {
+              if (a0) eval_group(Sc, j0, t * LPT + r, lo0, hi0, off0, m0, std::false_type{});
+              if (a1) eval_group(Sc, j1, (t + 1) * LPT + r, lo1, hi1, off1, m1, std::false_type{});
+            }
             emit_round(Sn, a0, lo0, hi0, off0, m0);
             if (jr1 < A) emit_round(Sn, a1, lo1, hi1, off1, m1);
             continue;
@@ -639,7 +644,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             } else {
               const bool act = j < A;
               std::uint32_t olo = 0, ohi = 0, off = 0, members = 1;
-              if (act) eval_group(Sc, j, (t + u) * LPT + r, olo, ohi, off, members, std::false_type{});
+              if constexpr (RG && !RG2 && LPT == 32 && kPlainShfl)
+                eval_group(Sc, act ? j : A - 1, (t + u) * LPT + r, olo, ohi, off, members, std::true_type{});
+              else if (act)
+                eval_group(Sc, j, (t + u) * LPT + r, olo, ohi, off, members, std::false_type{});
               emit_round(Sn, act, olo, ohi, off, members);
             }
           }
@@ -652,7 +660,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         const std::uint32_t g0 = gr + r, g1 = gr + LPT + r;
         const bool a0 = g0 < NG, a1 = g1 < NG;
         std::uint32_t lo0 = 0, hi0 = 0, off0 = 0, m0 = 1, lo1 = 0, hi1 = 0, off1 = 0, m1 = 1;
-        if constexpr (RG && LPT == 32 && kPlainShfl) {  // every lane evaluates (clamped), shuffles
+        if constexpr (RG && !RG2 && LPT == 32 && kPlainShfl) {  // every lane evaluates (clamped), shuffles
           eval_group(Sc, a0 ? g0 : NG - 1, 0, lo0, hi0, off0, m0, std::true_type{});
           eval_group(Sc, a1 ? g1 : NG - 1, 0, lo1, hi1, off1, m1, std::true_type{});
         } else {
@@ -858,7 +866,11 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches) {
-  const bool rg = lpt == 32 && h.rg_ok && h.n_single_alias >= 32;
+  // register gathers: one state word per lane (RG) whenever it fits — the
+  // single-node rounds and the uniform general / plain rounds use shuffles;
+  // two words per lane (RG2) only for the single-node rounds (general rounds
+  // keep the shared-memory gather: two shuffles per parent lose to it)
+  const bool rg = lpt == 32 && h.rg_ok;
   const bool rg2 = lpt == 32 && !h.rg_ok && h.sw32 <= 64 && h.n_single_alias >= 32 && kUseRg2;
   const int gm = rg2 ? 3 : !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
   const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm);
