@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool RG = GM >= 1;
   constexpr bool RG2 = GM == 3;
   constexpr bool SC = GM == 2;
+  // U53 compact kernels keep only the draws' high words in the chunk buffer
+  // (c2 +2.4 %; the general-path kernels lose 2-5 % to the recompute path)
+  constexpr bool HI = STREAM == STREAM_U53 && SC;
 
   const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
@@ -164,6 +167,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     return rp.pred.n != 0 && __all_sync(smask, ok) ? 1u : 0u;
   };
 
+  // the step's Philox constants and the first draw of the current phase-B
+  // chunk (the exact path recomputes a draw's low word from them)
+  step_philox sp{};
+  std::uint32_t jbase = 0;
+
   // Combined-function choice of alias group (engine.hpp:284-291) from draw jj
   // of the draw buffer, fast form: U53 integer cells (dev_plan.h a53) — `rare`
   // is set for draws on a cell boundary (about N in 2^32) and for launches or
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   auto alias_fast = [&](const uint4* cells, std::uint32_t asz, std::uint32_t ab,
                         std::uint32_t jj, bool& rare) -> std::uint32_t {
     if constexpr (STREAM == STREAM_U53) {
-      const std::uint32_t hi = dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
+      const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
       const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
       const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + e));  // {alias, hi32(C)}
@@ -190,7 +198,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
   // contraction, exactly as engine.hpp:285-290 computes it (U53 only).
   auto alias_exact = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
-    const raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+    raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+    if constexpr (HI) {  // the chunk keeps only the draws' high words: recompute the block
+      const std::uint32_t d = jbase + jj;  // draw index within the alias region
+      rw = pick53(philox_block(sp, nb0 + d / DPB, rp.rk0, rp.rk1), d % DPB);
+    }
     const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
     const double xx = __dmul_rn(u, __uint2double_rn(asz));
     std::uint32_t c = __double2uint_rz(xx);
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       const uint4 ar = ldp<GC>(arec4 + j);  // {U53 cell offset, function offset, N, ~N}
       std::uint32_t pick;
       if constexpr (STREAM == STREAM_U53) {
-        const std::uint32_t hi = dbuf[2 * jj + 1];
+        const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];
         const std::uint64_t P = static_cast<std::uint64_t>(hi) * ar.z;
         const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
         const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 8 * kScolSlots * e));
@@ -435,7 +447,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
 
   for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
     std::uint32_t* Sc = cur ? S1 : S0;
-    const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+    sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
 
     // ---- phase A: grouped perturbation + leaf draw (draws 0..g). Every draw
     // of a block is looked up; a per-draw mask keeps full patterns for draws
@@ -551,6 +563,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           xb[q] = philox_block(sp, nb0 + q * LPT + r, rp.rk0, rp.rk1);
       }
       for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB * CB) {
+        jbase = j0;
         if constexpr (!kPhiloxPipeline) {
 #pragma unroll
           for (std::uint32_t q = 0; q < CB; ++q)
@@ -558,8 +571,12 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         }
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
-          if (j0 + (q * LPT + r) * DPB < A)
-            *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
+          if (j0 + (q * LPT + r) * DPB < A) {
+            if constexpr (HI)  // high words only (the fast paths read r53 >> 21)
+              *reinterpret_cast<uint2*>(dbuf + 2 * (q * LPT + r)) = make_uint2(xb[q].y, xb[q].w);
+            else
+              *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
+          }
         __syncwarp(smask);
         if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
 #pragma unroll
