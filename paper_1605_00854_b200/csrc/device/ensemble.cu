@@ -571,12 +571,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         }
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
-          if (j0 + (q * LPT + r) * DPB < A) {
-            if constexpr (HI)  // high words only (the fast paths read r53 >> 21)
-              *reinterpret_cast<uint2*>(dbuf + 2 * (q * LPT + r)) = make_uint2(xb[q].y, xb[q].w);
-            else
-              *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
-          }
+          // (blocks past the region's last draw are stored too: never read)
+          if constexpr (HI)  // high words only (the fast paths read r53 >> 21)
+            *reinterpret_cast<uint2*>(dbuf + 2 * (q * LPT + r)) = make_uint2(xb[q].y, xb[q].w);
+          else
+            *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
         __syncwarp(smask);
         if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
 #pragma unroll
