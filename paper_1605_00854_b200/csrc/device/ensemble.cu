@@ -424,6 +424,27 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     }
   };
 
+  // Two single-node rounds (groups jr0 + r and jr0 + LPT + r, draws t*LPT + r
+  // and (t+1)*LPT + r of the chunk): both rounds' loads are issued before
+  // either ballot/store, so the two dependency chains overlap.
+  auto single_pair = [&](const std::uint32_t* Sc, std::uint32_t* Sn, std::uint32_t wreg,
+                         std::uint32_t jr0, std::uint32_t t) {
+    const std::uint32_t jr1 = jr0 + LPT;
+    bool rare0, rare1;
+    std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
+    std::uint32_t f1 = single_fn(jr1 + r, (t + 1) * LPT + r, rare1);
+    if constexpr (STREAM == STREAM_U53) {
+      if (__builtin_expect(rare0 || rare1, 0)) {
+        if (rare0) f0 = single_fn_exact(jr0 + r, t * LPT + r);
+        if (rare1) f1 = single_fn_exact(jr1 + r, (t + 1) * LPT + r);
+      }
+    }
+    const bool b0 = single_out(Sc, wreg, f0);
+    const bool b1 = single_out(Sc, wreg, f1);
+    store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
+    store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
+  };
+
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
   std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
@@ -562,7 +583,25 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t q = 0; q < CB; ++q)
           xb[q] = philox_block(sp, nb0 + q * LPT + r, rp.rk0, rp.rk1);
       }
-      for (std::uint32_t j0 = 0; j0 < A; j0 += LPT * DPB * CB) {
+      std::uint32_t jstart = 0;
+      if constexpr (SC && DPB * CB == 2 && !kPhiloxPipeline) {
+        // chunks made of one single-node round pair (U53 compact): no round
+        // bookkeeping; the general loop below takes the remaining chunks
+        const std::uint32_t jfull = A1 & ~(2u * LPT - 1u);
+        for (std::uint32_t j0 = 0; j0 < jfull; j0 += 2 * LPT) {
+          jbase = j0;
+          const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
+          if constexpr (HI)
+            *reinterpret_cast<uint2*>(dbuf + 2 * r) = make_uint2(x.y, x.w);
+          else
+            *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
+          __syncwarp(smask);
+          single_pair(Sc, Sn, wreg, j0, 0);
+          __syncwarp(smask);
+        }
+        jstart = jfull;
+      }
+      for (std::uint32_t j0 = jstart; j0 < A; j0 += LPT * DPB * CB) {
         jbase = j0;
         if constexpr (!kPhiloxPipeline) {
 #pragma unroll
@@ -612,19 +651,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
             }
           }
           if (jr1 + LPT <= A1) {
-            bool rare0, rare1;
-            std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
-            std::uint32_t f1 = single_fn(jr1 + r, (t + 1) * LPT + r, rare1);
-            if constexpr (STREAM == STREAM_U53) {
-              if (__builtin_expect(rare0 || rare1, 0)) {
-                if (rare0) f0 = single_fn_exact(jr0 + r, t * LPT + r);
-                if (rare1) f1 = single_fn_exact(jr1 + r, (t + 1) * LPT + r);
-              }
-            }
-            const bool b0 = single_out(Sc, wreg, f0);
-            const bool b1 = single_out(Sc, wreg, f1);
-            store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
-            store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
+            single_pair(Sc, Sn, wreg, jr0, t);
             continue;
           }
           // two general rounds: both groups' loads before either emit (not in
