@@ -115,7 +115,10 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // the function phase (c1: 0.37 -> +22%; c3: 0.91 -> -17%).
 constexpr double kScanBelow = 0.65;
 // Word-per-block phase A above this per-group flip probability.
-constexpr double kWordsAbove = 0.05;
+#ifndef PBN_WORDS_ABOVE
+#define PBN_WORDS_ABOVE 0.01
+#endif
+constexpr double kWordsAbove = PBN_WORDS_ABOVE;
 
 // Probability that a step reaches the function phase: no kept node flips
 // (every pattern draw returns 0, or every Bernoulli draw misses) and the leaf
@@ -253,8 +256,8 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
   if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
   rp.node_counts = nc ? d_node_counts : nullptr;
   // word-per-block phase A (U53): pays when groups flip often or a lane owns
-  // several phase-A blocks (c5: +2..11 % over p = 1e-4..0.1); with one block
-  // per lane and rare flips (c2) the per-draw path is ~1 % faster
+  // several phase-A blocks (c5: +2..11 % over p = 1e-4..0.1; c2, one block per
+  // lane and 1.6 % of groups flipping: +0.2 %)
   {
     const std::uint32_t lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
     const std::uint32_t blocks53 = (g.ep.h.g + g.ep.h.has_leaf + 1) / 2;
