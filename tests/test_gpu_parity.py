@@ -202,3 +202,15 @@ def test_node_one_counts_vs_oracle(pb, orc, cuda_ok, case, lpt):
     ost, ocnt, onc = orc.simulate(plan.view, 8, 0, n, steps, pred=pred, node_counts=True)
     assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
     assert np.array_equal(nc, onc)
+
+
+@pytest.mark.parametrize("lpt", [4, 8, 16, 32])
+@pytest.mark.parametrize("stream", [0, 1])
+def test_word_phase_a_any_lanes_per_trajectory(pb, orc, cuda_ok, lpt, stream):
+    """k=16 plan with frequent flips: the U53 word-per-block phase A on every
+    sub-warp width (U32 keeps the per-draw path)."""
+    plan, pred = _setup(pb, "c1_k16")
+    eng = pb.GpuEnsemble(plan, lanes_per_traj=lpt)
+    st, cnt = eng.simulate(seed=21, n_traj=90, n_steps=800, pred=pred, stream=stream)
+    ost, ocnt = orc.simulate(plan.view, 21, 0, 90, 800, pred=pred, stream=stream)
+    assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
