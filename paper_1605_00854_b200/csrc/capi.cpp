@@ -71,6 +71,13 @@ struct pbn_gpu {
   std::uint32_t last_warps = 0;
   std::uint32_t lpt_fixed = 0;  // 0: chosen per run
   std::uint32_t last_lpt = 0;
+  // device workspace of pbn_estimate, kept across calls (states, counts,
+  // carried samples, two pilot-series buffers, reduction scratch)
+  struct ws_buf {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+  };
+  ws_buf ws[6];
   double p_fn = 1.0;  // probability that a step reaches the function phase
   double p_group_flip = 0.0;  // probability that a full perturbation group flips
 };
@@ -659,6 +666,8 @@ void pbn_gpu_destroy(pbn_gpu* g) {
   if (g->d_blob) cudaFree(g->d_blob);
   if (g->d_states) cudaFree(g->d_states);
   if (g->d_counts) cudaFree(g->d_counts);
+  for (auto& b : g->ws)
+    if (b.p) cudaFree(b.p);
   delete g;
 }
 
@@ -741,6 +750,21 @@ struct dev_buf {
   void swap(dev_buf& o) { std::swap(p, o.p); }
 };
 
+// A workspace slot of the engine with room for n T's (grown, never shrunk).
+template <class T>
+T* ws_take(pbn_gpu& g, int slot, std::size_t n) {
+  auto& b = g.ws[slot];
+  const std::size_t bytes = sizeof(T) * (n ? n : 1);
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    ck(cudaMalloc(&b.p, bytes), "cudaMalloc workspace");
+    b.bytes = bytes;
+  }
+  return static_cast<T*>(b.p);
+}
+
 // Device ensemble: states, carried thin samples, pilot series and count
 // records stay in HBM; each round returns 8 pooled counters. The pilot series
 // buffer starts at the requested pilot length and grows (row copy) only when
@@ -755,11 +779,11 @@ class device_backend : public estimator_backend {
                                      std::max<std::uint64_t>(1024, (1ull << 33) / std::max(1u, req.n_traj)))),
         stride_(std::min<std::uint64_t>((cap_ + 31) / 32,
                                         (std::max<std::uint64_t>(req.pilot, 100) + 32) / 32)),
-        states_(static_cast<std::size_t>(req.n_traj) * words_),
-        counts_(static_cast<std::size_t>(req.n_traj) * PBN_COUNT_FIELDS),
-        tprev_(req.n_traj),
-        series_(static_cast<std::size_t>(req.n_traj) * stride_),
-        red_(16) {
+        states_{ws_take<std::uint64_t>(g, 0, static_cast<std::size_t>(req.n_traj) * words_)},
+        counts_{ws_take<std::uint64_t>(g, 1, static_cast<std::size_t>(req.n_traj) * PBN_COUNT_FIELDS)},
+        tprev_{ws_take<std::uint8_t>(g, 2, req.n_traj)},
+        series_{ws_take<std::uint32_t>(g, 3, static_cast<std::size_t>(req.n_traj) * stride_)},
+        red_{ws_take<unsigned long long>(g, 5, 16)} {
     ck(cudaMemset(series_.p, 0, sizeof(std::uint32_t) * req.n_traj * stride_), "memset");
   }
   std::uint32_t n_traj() const override { return req_.n_traj; }
@@ -775,12 +799,14 @@ class device_backend : public estimator_backend {
     const std::uint64_t need = (bits + 31) / 32;
     if (need <= stride_) return;
     const std::uint64_t stride = std::min<std::uint64_t>((cap_ + 31) / 32, std::max(need, 2 * stride_));
-    dev_buf<std::uint32_t> grown(static_cast<std::size_t>(req_.n_traj) * stride);
-    ck(cudaMemset(grown.p, 0, sizeof(std::uint32_t) * req_.n_traj * stride), "memset");
-    ck(cudaMemcpy2D(grown.p, 4 * stride, series_.p, 4 * stride_, 4 * stride_, req_.n_traj,
+    const int spare = series_slot_ == 3 ? 4 : 3;
+    std::uint32_t* grown = ws_take<std::uint32_t>(g_, spare, static_cast<std::size_t>(req_.n_traj) * stride);
+    ck(cudaMemset(grown, 0, sizeof(std::uint32_t) * req_.n_traj * stride), "memset");
+    ck(cudaMemcpy2D(grown, 4 * stride, series_.p, 4 * stride_, 4 * stride_, req_.n_traj,
                     cudaMemcpyDeviceToDevice),
        "series grow");
-    series_.swap(grown);
+    series_.p = grown;
+    series_slot_ = spare;
     stride_ = stride;
   }
   void run(std::uint64_t step_begin, std::uint64_t n_steps, std::uint32_t kappa,
@@ -834,10 +860,16 @@ class device_backend : public estimator_backend {
   const std::uint8_t* vals_;
   std::uint32_t n_pred_;
   std::uint64_t words_, cap_, stride_;
-  dev_buf<std::uint64_t> states_, counts_;
-  dev_buf<std::uint8_t> tprev_;
-  dev_buf<std::uint32_t> series_;
-  dev_buf<unsigned long long> red_;
+  // views of the engine's workspace slots (pbn_gpu::ws)
+  template <class T>
+  struct view {
+    T* p;
+  };
+  view<std::uint64_t> states_, counts_;
+  view<std::uint8_t> tprev_;
+  view<std::uint32_t> series_;
+  view<unsigned long long> red_;
+  int series_slot_ = 3;
 };
 
 class callback_backend : public estimator_backend {
