@@ -71,13 +71,14 @@ struct pbn_gpu {
   std::uint32_t last_warps = 0;
   std::uint32_t lpt_fixed = 0;  // 0: chosen per run
   std::uint32_t last_lpt = 0;
-  // device workspace of pbn_estimate, kept across calls (states, counts,
-  // carried samples, two pilot-series buffers, reduction scratch)
+  // device workspace kept across calls: pbn_estimate's states, counts,
+  // carried samples, two pilot-series buffers and reduction scratch (0-5);
+  // pbn_gpu_run's carried samples, series and node counts (6-8)
   struct ws_buf {
     void* p = nullptr;
     std::size_t bytes = 0;
   };
-  ws_buf ws[6];
+  ws_buf ws[9];
   double p_fn = 1.0;  // probability that a step reaches the function phase
   double p_group_flip = 0.0;  // probability that a full perturbation group flips
 };
@@ -216,6 +217,21 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
   while (w > 1 && w * per_warp > avail) --w;
   if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
   return static_cast<std::uint32_t>(w);
+}
+
+// A workspace slot of the engine with room for n T's (grown, never shrunk).
+template <class T>
+T* ws_take(pbn_gpu& g, int slot, std::size_t n) {
+  auto& b = g.ws[slot];
+  const std::size_t bytes = sizeof(T) * (n ? n : 1);
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    ck(cudaMalloc(&b.p, bytes), "cudaMalloc workspace");
+    b.bytes = bytes;
+  }
+  return static_cast<T*>(b.p);
 }
 
 dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
@@ -610,32 +626,21 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* c
     std::uint8_t* d_tprev = nullptr;
     std::uint32_t* d_series = nullptr;
     const std::size_t series_bytes = 4 * a->series_stride * a->n_traj;
-    struct scratch {
-      void* p = nullptr;
-      ~scratch() { if (p) cudaFree(p); }
-    } s1, s2;
     if (a->tprev) {
-      ck(cudaMalloc(&d_tprev, a->n_traj), "cudaMalloc tprev");
-      s1.p = d_tprev;
+      d_tprev = ws_take<std::uint8_t>(*g, 6, a->n_traj);
       ck(cudaMemcpy(d_tprev, a->tprev, a->n_traj, cudaMemcpyHostToDevice), "H2D");
       da.tprev = d_tprev;
     }
     if (a->series) {
-      ck(cudaMalloc(&d_series, series_bytes), "cudaMalloc series");
-      s2.p = d_series;
+      d_series = ws_take<std::uint32_t>(*g, 7, series_bytes / 4);
       ck(cudaMemcpy(d_series, a->series, series_bytes, cudaMemcpyHostToDevice), "H2D");
       da.series = d_series;
     }
     std::uint64_t* d_nc = nullptr;
-    struct scratch3 {
-      void* p = nullptr;
-      ~scratch3() { if (p) cudaFree(p); }
-    } s3;
     const std::size_t nc_bytes = 8ull * g->ep.h.n_kept * a->n_traj;
     if (a->flags & PBN_RUN_NODE_COUNTS) {
       need(node_counts, "node_counts");
-      ck(cudaMalloc(&d_nc, nc_bytes), "cudaMalloc node counts");
-      s3.p = d_nc;
+      d_nc = ws_take<std::uint64_t>(*g, 8, nc_bytes / 8);
       ck(cudaMemset(d_nc, 0, nc_bytes), "memset");
     }
     run_device(*g, da, g->d_states, g->d_counts, d_nc, nullptr);
@@ -749,21 +754,6 @@ struct dev_buf {
   dev_buf& operator=(const dev_buf&) = delete;
   void swap(dev_buf& o) { std::swap(p, o.p); }
 };
-
-// A workspace slot of the engine with room for n T's (grown, never shrunk).
-template <class T>
-T* ws_take(pbn_gpu& g, int slot, std::size_t n) {
-  auto& b = g.ws[slot];
-  const std::size_t bytes = sizeof(T) * (n ? n : 1);
-  if (b.bytes < bytes) {
-    if (b.p) cudaFree(b.p);
-    b.p = nullptr;
-    b.bytes = 0;
-    ck(cudaMalloc(&b.p, bytes), "cudaMalloc workspace");
-    b.bytes = bytes;
-  }
-  return static_cast<T*>(b.p);
-}
 
 // Device ensemble: states, carried thin samples, pilot series and count
 // records stay in HBM; each round returns 8 pooled counters. The pilot series
