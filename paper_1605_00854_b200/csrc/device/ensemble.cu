@@ -445,6 +445,28 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     store_bits(Sn, jr1, __ballot_sync(smask, b1), true);
   };
 
+  // Four single-node rounds at once (U32 compact: a chunk of 4-draw blocks):
+  // four independent chains.
+  auto single_quad = [&](const std::uint32_t* Sc, std::uint32_t* Sn, std::uint32_t wreg,
+                         std::uint32_t jr0, std::uint32_t t) {
+    bool rr[4];
+    std::uint32_t f[4];
+#pragma unroll
+    for (std::uint32_t u = 0; u < 4; ++u) f[u] = single_fn(jr0 + u * LPT + r, (t + u) * LPT + r, rr[u]);
+    if constexpr (STREAM == STREAM_U53) {
+      if (__builtin_expect(rr[0] || rr[1] || rr[2] || rr[3], 0)) {
+#pragma unroll
+        for (std::uint32_t u = 0; u < 4; ++u)
+          if (rr[u]) f[u] = single_fn_exact(jr0 + u * LPT + r, (t + u) * LPT + r);
+      }
+    }
+    bool b[4];
+#pragma unroll
+    for (std::uint32_t u = 0; u < 4; ++u) b[u] = single_out(Sc, wreg, f[u]);
+#pragma unroll
+    for (std::uint32_t u = 0; u < 4; ++u) store_bits(Sn, jr0 + u * LPT, __ballot_sync(smask, b[u]), true);
+  };
+
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
   std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
@@ -600,6 +622,17 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           __syncwarp(smask);
         }
         jstart = jfull;
+      } else if constexpr (SC && DPB * CB == 4 && kQuadRounds && !kPhiloxPipeline) {
+        // U32 compact: chunks of one single-node quad
+        const std::uint32_t jfull = A1 & ~(4u * LPT - 1u);
+        for (std::uint32_t j0 = 0; j0 < jfull; j0 += 4 * LPT) {
+          jbase = j0;
+          *reinterpret_cast<uint4*>(dbuf + 4 * r) = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
+          __syncwarp(smask);
+          single_quad(Sc, Sn, wreg, j0, 0);
+          __syncwarp(smask);
+        }
+        jstart = jfull;
       }
       for (std::uint32_t j0 = jstart; j0 < A; j0 += LPT * DPB * CB) {
         jbase = j0;
@@ -630,22 +663,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           if constexpr (kQuadRounds && SC && DPB * CB >= 4) {
             // four single-node rounds at once: four independent chains
             if ((t & 3) == 0 && jr0 + 4 * LPT <= A1) {
-              bool rr[4];
-              std::uint32_t f[4];
-#pragma unroll
-              for (std::uint32_t u = 0; u < 4; ++u) f[u] = single_fn(jr0 + u * LPT + r, (t + u) * LPT + r, rr[u]);
-              if constexpr (STREAM == STREAM_U53) {
-                if (__builtin_expect(rr[0] || rr[1] || rr[2] || rr[3], 0)) {
-#pragma unroll
-                  for (std::uint32_t u = 0; u < 4; ++u)
-                    if (rr[u]) f[u] = single_fn_exact(jr0 + u * LPT + r, (t + u) * LPT + r);
-                }
-              }
-              bool b[4];
-#pragma unroll
-              for (std::uint32_t u = 0; u < 4; ++u) b[u] = single_out(Sc, wreg, f[u]);
-#pragma unroll
-              for (std::uint32_t u = 0; u < 4; ++u) store_bits(Sn, jr0 + u * LPT, __ballot_sync(smask, b[u]), true);
+              single_quad(Sc, Sn, wreg, jr0, t);
               t += 2;  // with the loop's += 2: next quad
               continue;
             }
