@@ -257,10 +257,31 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
             leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
         }
       };
-      for (std::uint32_t b = 0; b < nplain; ++b) {
-        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+      if (!BERN && k * DPB == 32) {
+        // k * DPB == 32: a plain block's patterns fill exactly state word b —
+        // OR them and XOR the word once
+        constexpr std::uint32_t K = 32 / DPB;
+        for (std::uint32_t b = 0; b < nplain; ++b) {
+          const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+          std::uint32_t wd = 0;
 #pragma unroll
-        for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, false);
+          for (std::uint32_t e = 0; e < DPB; ++e) {
+            if constexpr (STREAM == STREAM_U53)
+              wd |= pert_draw53<GP>(pert53, pick53(x, e), K) << (e * K);
+            else
+              wd |= pert_draw32<GP>(pert32, pick32(x, e), K) << (e * K);
+          }
+          if (__builtin_expect(wd != 0, 0)) {
+            flip = true;
+            Sc[32 * b] ^= wd;
+          }
+        }
+      } else {
+        for (std::uint32_t b = 0; b < nplain; ++b) {
+          const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+#pragma unroll
+          for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, false);
+        }
       }
       for (std::uint32_t b = nplain; b < nb0; ++b) {
         const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
