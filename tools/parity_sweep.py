@@ -32,7 +32,7 @@ for case in range(n_cases):
         print(f"case {case}: skip ({type(e).__name__})")
         continue
     pred = plan.compile_predicate(terms)
-    lpt = int(rng.choice([0, 0, 1, 8, 32]))
+    lpt = int(rng.choice([0, 0, 1, 2, 4, 8, 16, 32]))
     if lpt == 1 and plan.n_kept > 255:
         lpt = 0
     stream = int(rng.integers(0, 2))
