@@ -115,7 +115,9 @@ typedef struct pbn_plan_view {
   uint64_t n_table;
   const uint64_t* fn_tables;       /* packed member outputs (member 0 = bit 0)               */
   /* Stepper kind. Grouped plans (pbn_prepare): pert_mode 0 (g pattern draws
-   * through the 2^k alias cells), has_leaf 1, grp_members NULL (member counts
+   * through the 2^k alias cells), has_leaf 1 — REQUIRED: the grouped stepper
+   * always makes the leaf draw (engine.hpp:268), so pbn_gpu_create rejects
+   * pert_mode 0 with has_leaf 0 (PBN_EUSAGE) — grp_members NULL (member counts
    * follow from the offsets). Node-wise plans (pbn_prepare_nodewise, the
    * reference's Method_old / Method_reduction steppers, engine.hpp:168-242):
    * pert_mode 1 (g = n per-node Bernoulli(pert_p) draws, flip iff u < p),
@@ -216,7 +218,9 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lanes_per_tra
  * truth tables in smem, 4 everything (incl. perturbation cells) in smem, 5 core +
  * the perturbation cells in smem (tables through L1/L2).
  * PBN_ERESOURCE if it does not fit. pbn_gpu_info reports the level as
- * (placement code - 1): 0 global, 1 core, 2 tables, 3 all, 4 core + cells. */
+ * (placement code - 1): 0 global, 1 core, 2 tables, 3 all, 4 core + cells —
+ * after a run, the level that run's launch actually used (a run steps down
+ * when the ensemble's per-trajectory state does not fit next to the plan). */
 int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement);
 int pbn_gpu_info(const pbn_gpu* g, uint32_t* lanes_per_traj, uint32_t* tables_in_smem,
                  uint64_t* smem_bytes, uint64_t* plan_bytes, uint32_t* warps_per_cta);

@@ -480,6 +480,12 @@ class GpuEnsemble:
 
     def __init__(self, plan, device: int = 0, lanes_per_traj: int = 0, placement: str = "auto"):
         view = plan.view if isinstance(plan, PreparedSimulation) else plan
+        if not isinstance(view, PlanView):
+            # any structure with the pbn_plan_view layout (e.g. a reference-side
+            # view of pbn::prepare's plan, oracle/_ref): reinterpret, no copy
+            if C.sizeof(view) != C.sizeof(PlanView):
+                raise UsageError("plan view layout does not match pbn_plan_view")
+            view = C.cast(C.pointer(view), C.POINTER(PlanView)).contents
         self._keep = plan  # the view's arrays must outlive creation
         self.n_kept = view.n_kept
         self.words = state_words(self.n_kept)

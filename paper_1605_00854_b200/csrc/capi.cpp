@@ -71,6 +71,7 @@ struct pbn_gpu {
   std::uint32_t last_warps = 0;
   std::uint32_t lpt_fixed = 0;  // 0: chosen per run
   std::uint32_t last_lpt = 0;
+  int last_place = -1;  // placement the last launch actually ran (-1: none yet)
   // device workspace kept across calls: pbn_estimate's states, counts,
   // carried samples, two pilot-series buffers and reduction scratch (0-5);
   // pbn_gpu_run's carried samples, series and node counts (6-8)
@@ -310,6 +311,7 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
                                  g.p_fn < kScanBelow, g.last_warps, rp, d_states, d_counts, stream, &g.launches)
           : launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_lpt,
                             g.last_warps, rp, d_states, d_counts, stream, &g.launches);
+  g.last_place = g.place;
   g.place = place0;
   ck(e, "ensemble launch");
 }
@@ -593,8 +595,11 @@ int pbn_gpu_info(const pbn_gpu* g, uint32_t* lpt, uint32_t* tables_in_smem, uint
   return guard([&] {
     need(g, "gpu");
     if (lpt) *lpt = g->last_lpt ? g->last_lpt : g->lpt_fixed;
-    if (tables_in_smem) *tables_in_smem = static_cast<uint32_t>(g->place);
-    if (smem_bytes) *smem_bytes = staged_bytes(*g);
+    // the placement the last launch ran (run_device may step down from the
+    // configured one when the ensemble's state does not fit next to it)
+    const int place = g->last_place >= 0 ? g->last_place : g->place;
+    if (tables_in_smem) *tables_in_smem = static_cast<uint32_t>(place);
+    if (smem_bytes) *smem_bytes = staged_bytes_at(g->ep.h, place);
     if (plan_bytes) *plan_bytes = g->ep.blob.size();
     if (warps_per_cta) *warps_per_cta = g->last_warps;
   });

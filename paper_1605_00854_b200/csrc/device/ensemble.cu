@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   std::uint32_t* planes = dbuf + kBuf;   // node counts: plane i of word w at [8*w + i]
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
-    for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w];
+    for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w] & state_word_mask(h.n_kept, w);
     if (rp.node_counts)
       for (std::uint32_t w = r; w < sw32; w += LPT)
 #pragma unroll
@@ -592,6 +592,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       // ---- function phase, in lockstep rounds of LPT groups
       std::uint32_t* Sn = cur ? S0 : S1;
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
+      // the zeroing must be visible to the other lanes' ORs (shuffles and
+      // votes do not order shared memory; a plan without alias groups goes
+      // straight to the plain region's atomics)
+      __syncwarp(smask);
       std::uint32_t wreg = 0;  // RG: state word `lane` of the current state
       if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
       wreg_s = wreg;

@@ -124,6 +124,14 @@ __device__ __forceinline__ const std::uint8_t* pert_cells(const std::uint8_t* sm
   return gblob + pert_off<STREAM>(h);
 }
 
+// Valid bits of 32-bit state word w of an n-bit state: bits at and above n
+// (the slack bit n' that padded gather slots read, and the rest of the last
+// word) must be zero, so a caller's stray high bits are cleared on load.
+__device__ __forceinline__ std::uint32_t state_word_mask(std::uint32_t n, std::uint32_t w) {
+  const std::uint32_t lo = 32 * w;
+  return lo + 32 <= n ? 0xFFFFFFFFu : lo >= n ? 0u : (1u << (n - lo)) - 1u;
+}
+
 template <int STREAM>
 struct draws {
   static constexpr std::uint32_t kPerBlock = STREAM == STREAM_U53 ? 2 : 4;

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   std::uint32_t cur = 0;                          // current state buffer (per lane)
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
-    for (std::uint32_t w = 0; w < sw32; ++w) wbuf[32 * w] = src[w];
+    for (std::uint32_t w = 0; w < sw32; ++w) wbuf[32 * w] = src[w] & state_word_mask(h.n_kept, w);
     if (rp.node_counts)
       for (std::uint32_t i = 0; i < 8 * sw32; ++i) planes[32 * i] = 0;
   }

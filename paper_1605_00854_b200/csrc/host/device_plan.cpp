@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
 #include <cstring>
 #include <string>
 
@@ -143,6 +144,13 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   h.n_groups = v.n_groups;
   h.rg_ok = h.sw32 <= 32 ? 1u : 0u;
   if (v.pert_mode > 1) throw model_error("unknown perturbation mode");
+  // The grouped stepper always makes the leaf draw once no kept node flipped
+  // (engine.hpp:268, also when t == 1); a grouped view without it would shift
+  // every function-selection draw by one. Only Method_old (pert_mode 1) has
+  // no leaf draw (engine.hpp:193-201).
+  if (v.pert_mode == 0 && !v.has_leaf)
+    throw std::invalid_argument(
+        "plan view: grouped plans (pert_mode 0) need has_leaf = 1 (engine.hpp:268)");
   h.pert_mode = v.pert_mode;
   h.has_leaf = v.has_leaf ? 1u : 0u;
   if (v.pert_mode == 1) {
