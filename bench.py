@@ -27,9 +27,33 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import gzip  # noqa: E402
+
 import numpy as np  # noqa: E402
 
-from paper_1605_00854_b200.configs import CONFIGS  # noqa: E402
+# The workload table and model texts are plain files (workloads/): the
+# reference arm reads them without importing the engine package, so its
+# process never maps libpbn_b200.so.
+WORKLOADS_DIR = os.path.join(ROOT, "workloads")
+with open(os.path.join(WORKLOADS_DIR, "workloads.json")) as _f:
+    WORKLOADS = json.load(_f)
+
+
+def workload_text(name, p=None):
+    """Committed model text of a workload (workloads/<name>.pbn.gz), with the
+    perturbation rate replaced when `p` is given (the c5 sweep): the generator
+    draws the network independently of p and the serialiser prints p with
+    %.12g (io.hpp:199-203), so this equals the generator's text at that p
+    (tests/test_workloads.py)."""
+    with gzip.open(os.path.join(WORKLOADS_DIR, f"{name}.pbn.gz"), "rt") as f:
+        text = f.read()
+    if p is not None:
+        lines = text.split("\n")
+        assert lines[1].startswith("perturbation ")
+        lines[1] = f"perturbation {p:.12g}"
+        text = "\n".join(lines)
+    return text
+
 
 METRIC = "node-updates/sec"
 UNIT = "node-updates/s"
@@ -41,7 +65,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--stream", default="u53", choices=["u53", "u32"])
     ap.add_argument("--p", type=float, default=None, help="override perturbation rate (c5 sweep)")
     ap.add_argument("--traj", type=int, default=None, help="trajectories per GPU")
@@ -68,19 +92,20 @@ def dist_env():
 
 
 def build_workload(cfg, p_override, method="grouped", k=None, mgp=None):
-    """Model text is the interchange format: both this library and the
-    reference parse the same text, so their plans are bitwise identical."""
+    """Model text is the interchange format: both arms parse the same committed
+    text (workloads/<cfg>.pbn.gz), so their plans are bitwise identical."""
     import dataclasses
 
     import paper_1605_00854_b200 as pb
+    from paper_1605_00854_b200.configs import CONFIGS
 
     w = CONFIGS[cfg]
     if k is not None:
         w = dataclasses.replace(w, k_max=k)
     if mgp is not None:
         w = dataclasses.replace(w, mgp=mgp)
-    model, terms = w.model(p_override)
-    text = model.serialize()
+    text = workload_text(cfg, p_override)
+    terms = [tuple(t) for t in WORKLOADS[cfg]["terms"]]
     model = pb.parse_model(text)
     if method == "grouped":
         plan = pb.prepare(model, w.theta, w.k_max, w.mgp)
@@ -155,10 +180,21 @@ def measured_peaks():
 METHOD_CODE = {"grouped": 0, "old": 1, "reduction": 2}
 
 
-def cpu_reference_rate(text, w, terms, seconds, threads=None, method="grouped"):
+def ref_ensemble_sample(rplan, pred, n_traj, seconds, threads, method_code):
+    """Steps per trajectory so that the reference stepper (oracle/_ref) runs the
+    ensemble's n_traj trajectories in about `seconds` on `threads` threads."""
+    cal = min(n_traj, 4 * threads)
+    rplan.bench_ensemble(41, threads, cal, 200, pred, method_code)  # cold: threads, pages
+    t, _ = rplan.bench_ensemble(42, threads, cal, 1000, pred, method_code)
+    per_traj_step = max(t / 1000 * threads / cal, 1e-10)  # thread-seconds
+    return max(500, int(seconds * threads / (per_traj_step * n_traj)))
+
+
+def cpu_reference_rate(text, w, terms, seconds, n_traj, threads=None, method="grouped"):
     """The unmodified reference stepper (oracle/_ref, xoshiro256) — grouped,
-    Method_old or Method_reduction — one trajectory per host thread.
-    Returns (traj-steps/s, threads, steps, seconds, state bits)."""
+    Method_old or Method_reduction — on the GPU arm's ensemble: all n_traj
+    trajectories, a bounded number of steps each, over every host thread.
+    Returns (traj-steps/s, threads, steps per trajectory, seconds, state bits)."""
     import oracle
 
     ref = oracle.Reference()
@@ -167,13 +203,9 @@ def cpu_reference_rate(text, w, terms, seconds, threads=None, method="grouped"):
     pred = rplan.compile_predicate(terms)
     threads = threads or os.cpu_count() or 1
     code = METHOD_CODE[method]
-    # calibrate on one thread, then size the sample to ~`seconds`
-    s_cal = 2000
-    t, _ = rplan.bench_xoshiro(42, 1, s_cal, pred, code)
-    per_step = max(t / s_cal, 1e-9)
-    steps = max(1000, int(seconds / per_step))
-    t, _ = rplan.bench_xoshiro(42, threads, steps, pred, code)
-    rate = threads * steps / t
+    steps = ref_ensemble_sample(rplan, pred, n_traj, seconds, threads, code)
+    t, _ = rplan.bench_ensemble(42, threads, n_traj, steps, pred, code)
+    rate = n_traj * steps / t
     n_state = {"grouped": rplan.n_kept, "reduction": rplan.n_kept}.get(method, w.n)
     return rate, threads, steps, t, n_state
 
@@ -213,43 +245,77 @@ def reference_estimate_arm(a, w, rplan, terms, threads):
 
 
 def run_reference_arm(a):
+    """The reference's own CPU implementation of the path: the unmodified
+    grouped_simulator + xoshiro256 (oracle/_ref/libpbnref.so, built from
+    /root/reference's headers) on every host thread, over the same workload
+    text and plan as the GPU arm — all of the ensemble's trajectories, a
+    bounded number of steps each. Imports `oracle` only: the engine library is
+    never loaded in this process."""
     rank, world, local = dist_env()
     if rank != 0:
         return
-    import paper_1605_00854_b200 as pb  # noqa: F401  (model generation / plan only)
-
-    w, text, model, plan, terms = build_workload(a.config, a.p, "grouped", a.k, a.mgp)
     import oracle
 
+    wd = WORKLOADS[a.config]
+    p = a.p if a.p is not None else wd["p"]
+    text = workload_text(a.config, a.p)
+    terms = [tuple(t) for t in wd["terms"]]
+    theta = wd["theta"]
+    k = a.k if a.k is not None else wd["k_max"]
+    mgp = a.mgp if a.mgp is not None else wd["mgp"]
     ref = oracle.Reference()
-    rplan = ref.parse(text).prepare(w.theta, w.k_max, w.mgp)
+    rmodel = ref.parse(text)
+    rplan = rmodel.prepare(theta, k, mgp)
     pred = rplan.compile_predicate(terms)
     threads = os.cpu_count() or 1
-    if w.n_steps == 0:
-        return reference_estimate_arm(a, w, rplan, terms, threads)
-    t, _ = rplan.bench_xoshiro(42, 1, 2000, pred)
-    steps = max(1000, int(6.0 / max(t / 2000, 1e-9)))  # ~6 s per bench step
+
+    class _W:  # the fields reference_estimate_arm reads
+        n = wd["n"]
+        note = wd["note"]
+
+    if wd["n_steps"] == 0:
+        return reference_estimate_arm(a, _W, rplan, terms, threads)
+    n_traj = a.traj or wd["n_traj"]
+    steps = ref_ensemble_sample(rplan, pred, n_traj, 6.0, threads, 0)  # ~6 s per bench step
     for _ in range(a.warmup):
-        rplan.bench_xoshiro(42, threads, max(1000, steps // 10), pred)
+        rplan.bench_ensemble(7, threads, n_traj, max(20, steps // 10), pred)
     times = []
-    for k in range(a.steps):
-        t, _ = rplan.bench_xoshiro(42 + 1000 * k, threads, steps, pred)
+    for kk in range(a.steps):
+        t, _ = rplan.bench_ensemble(42 + 1000 * kk, threads, n_traj, steps, pred)
         times.append(t)
     total = sum(times)
-    tsteps = threads * steps * a.steps
+    tsteps = n_traj * steps * a.steps
     val = tsteps * rplan.n_kept / total
+    # the same ensemble at the reference's default plan (engine.hpp:81-83:
+    # theta 2^25, k 16, mgp 18), a shorter sample, reported beside it
+    default_plan = {"plan": {"theta": 1 << 25, "k_max": 16, "mgp": 18}}
+    try:
+        dplan = rmodel.prepare(1 << 25, 16, 18)
+        dpred = dplan.compile_predicate(terms)
+        dsteps = ref_ensemble_sample(dplan, dpred, n_traj, 3.0, threads, 0)
+        dt, _ = dplan.bench_ensemble(42, threads, n_traj, dsteps, dpred)
+        default_plan.update({"value": n_traj * dsteps * dplan.n_kept / dt, "unit": UNIT,
+                             "trajectory_steps_per_s": n_traj * dsteps / dt,
+                             "sample": f"{n_traj} trajectories x {dsteps} steps"})
+    except oracle.RefError as e:  # e.g. c4: the default mgp does not plan
+        default_plan["error"] = str(e)
     line = {
         "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1000 * total / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"{a.config}: {w.note}", "n": w.n, "n_kept": rplan.n_kept,
-                   "plan": {"theta": w.theta, "k_max": w.k_max, "mgp": w.mgp},
-                   "p": a.p if a.p is not None else w.p},
+        "config": {"workload": f"{a.config}: {wd['note']}", "n": wd["n"], "n_kept": rplan.n_kept,
+                   "method": "grouped", "trajectories_per_gpu": n_traj,
+                   "sim_steps_sampled_per_trajectory": steps,
+                   "p": p, "plan": {"theta": theta, "k_max": k, "mgp": mgp},
+                   "model": f"workloads/{a.config}.pbn.gz"},
         "trajectory_steps_per_s": tsteps / total,
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{threads} threads x {steps} steps, reference grouped_simulator"
-                                   f" + xoshiro256, count_nodes=false, predicate on"},
+                         "sample": f"all {n_traj} trajectories x {steps} steps per bench step "
+                                   f"(the GPU arm runs {wd['n_steps']}), unmodified reference "
+                                   f"grouped_simulator + xoshiro256, count_nodes=false, "
+                                   f"predicate on, {threads} threads"},
+        "reference_default_plan": default_plan,
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -363,7 +429,7 @@ def run_ours(a):
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if a.mode == "estimate" or (a.mode == "auto" and CONFIGS[a.config].n_steps == 0):
+    if a.mode == "estimate" or (a.mode == "auto" and WORKLOADS[a.config]["n_steps"] == 0):
         run_estimate_mode(a, torch, dist if world > 1 else None, rank, world, local, dev)
         if world > 1:
             dist.destroy_process_group()
@@ -552,11 +618,12 @@ def run_ours(a):
     if not a.no_cpu_baseline and world == 1:
         try:
             rate, threads, steps, secs, nk = cpu_reference_rate(text, w, terms, a.cpu_seconds,
-                                                                method=a.method)
+                                                                n_traj, method=a.method)
             line["cpu_baseline"] = {
                 "value": rate * nk, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{threads} threads x {steps} steps ({secs:.1f} s), unmodified reference "
-                          f"{a.method} stepper + xoshiro256 (oracle/_ref)",
+                "sample": f"all {n_traj} trajectories x {steps} steps ({secs:.1f} s) on {threads} "
+                          f"threads, unmodified reference {a.method} stepper + xoshiro256 "
+                          f"(oracle/_ref)",
                 "trajectory_steps_per_s": rate}
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(e)}

@@ -181,6 +181,7 @@ class Reference:
             "ref_simulate_nodewise": (I, [P, I, U64, U64, U32, I, U64, U64, PU32, PU8, U32, PU64,
                                           PU64, PU64]),
             "ref_bench_xoshiro": (I, [P, U64, U32, U64, PU32, PU8, U32, I, P, PD, PU64]),
+            "ref_bench_ensemble": (I, [P, U64, U32, U32, U64, PU32, PU8, U32, I, P, PD, PU64]),
             "ref_estimate": (I, [P, PU32, PU8, U32, D, D, U64, U64, I, U32, PD, PU64, PU64,
                                  C.POINTER(C.c_int)]),
             "ref_exact_matrix": (I, [P, D, PD]),
@@ -353,6 +354,20 @@ class RefPlan:
         self.ref._ck(self.ref.lib.ref_bench_xoshiro(self._h, seed, n_threads, steps_per_thread,
                                                     _u32p(bits), _u8p(vals), npred, method,
                                                     self.model._h, C.byref(secs), C.byref(hits)))
+        return secs.value, hits.value
+
+    def bench_ensemble(self, seed, n_threads, n_traj, steps, pred=None, method=0):
+        """CPU baseline on an ensemble: n_traj trajectories x steps, dealt to
+        n_threads threads (reference stepper + xoshiro256 seeded seed + id)."""
+        bits = np.zeros(1, np.uint32) if pred is None else np.ascontiguousarray(pred[0], np.uint32)
+        vals = np.zeros(1, np.uint8) if pred is None else np.ascontiguousarray(pred[1], np.uint8)
+        npred = 0 if pred is None else len(pred[0])
+        secs = C.c_double()
+        hits = C.c_uint64()
+        self.ref._ck(self.ref.lib.ref_bench_ensemble(self._h, seed, n_threads, n_traj, steps,
+                                                     _u32p(bits), _u8p(vals), npred, method,
+                                                     self.model._h, C.byref(secs),
+                                                     C.byref(hits)))
         return secs.value, hits.value
 
     def grouped_row(self, e):

@@ -429,6 +429,64 @@ int ref_bench_xoshiro(void* p, std::uint64_t seed, std::uint32_t n_threads,
   });
 }
 
+// The CPU reference on the GPU arm's ensemble shape: n_traj independent
+// trajectories (all-zero initial states, pbn_main.cpp:232; xoshiro256 seeded
+// seed + trajectory id), each advanced `steps` steps by the unmodified
+// stepper, dealt round-robin to n_threads host threads (harness-level
+// parallelism only; the plan is shared, const). method as ref_bench_xoshiro.
+int ref_bench_ensemble(void* p, std::uint64_t seed, std::uint32_t n_threads,
+                       std::uint32_t n_traj, std::uint64_t steps, const std::uint32_t* pred_bits,
+                       const std::uint8_t* pred_vals, std::uint32_t n_pred, int method,
+                       const void* model, double* seconds_out, std::uint64_t* hits_out) {
+  return guarded([&] {
+    const auto& ps = static_cast<ref_plan*>(p)->ps;
+    pbn::compiled_predicate cp;
+    for (std::uint32_t i = 0; i < n_pred; ++i) cp.emplace_back(pred_bits[i], pred_vals[i] != 0);
+    std::atomic<std::uint32_t> ready{0};
+    std::atomic<bool> go{false};
+    std::vector<std::uint64_t> hits(n_threads, 0);
+    std::vector<std::thread> th;
+    for (std::uint32_t i = 0; i < n_threads; ++i) {
+      th.emplace_back([&, i] {
+        pbn::sim_options opt;
+        opt.count_nodes = false;  // bench.hpp:116-124
+        opt.predicate = (method == 0 && n_pred) ? &cp : nullptr;
+        ready.fetch_add(1);
+        while (!go.load()) {
+        }
+        std::uint64_t h = 0;
+        for (std::uint32_t t = i; t < n_traj; t += n_threads) {
+          pbn::xoshiro256 rng(seed + t);
+          if (method == 0) {
+            pbn::grouped_simulator sim(ps);
+            pbn::state s(sim.state_bits());
+            h += pbn::simulate(sim, s, steps, rng, opt).predicate_hits;
+          } else if (method == 1) {
+            pbn::reference_simulator sim(*static_cast<const pbn::model*>(model));
+            pbn::state s(sim.state_bits());
+            h += pbn::simulate(sim, s, steps, rng, opt).steps;
+          } else {
+            pbn::reduced_simulator sim(ps.reduced);
+            pbn::state s(sim.state_bits());
+            h += pbn::simulate(sim, s, steps, rng, opt).steps;
+          }
+        }
+        hits[i] = h;
+      });
+    }
+    while (ready.load() != n_threads) {
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    go.store(true);
+    for (auto& t : th) t.join();
+    *seconds_out =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::uint64_t h = 0;
+    for (auto x : hits) h += x;
+    *hits_out = h;
+  });
+}
+
 std::uint64_t ref_last_estimate_steps() { return g_last_estimate_steps; }
 
 // Reference two-state estimator (estimator.hpp:137-244) on one trajectory.
