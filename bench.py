@@ -55,6 +55,11 @@ def workload_text(name, p=None):
     return text
 
 
+# Philox4x32-10 blocks/s of a Philox-only kernel of this engine on one B200
+# (tools/ceilings.cu, 416 blocks per step, 4144 warps; profiles/r02_ceilings.jsonl):
+# the 32x32->64 multiplies (IMAD.WIDE, 17 per block) bound it, not issue
+PHILOX_BLOCKS_PER_S = 4.797e11
+
 METRIC = "node-updates/sec"
 UNIT = "node-updates/s"
 
@@ -557,15 +562,17 @@ def run_ours(a):
     peak_lookups = props.multi_processor_count * 32 * sm_mhz * 1e6
     lookups = flat.expected_lookups(fn_total, traj_steps)
     achieved = lookups / (total_ms / 1e3) / world
-    # Ceiling the injected stream imposes: a kernel issuing
-    # nothing but the Philox4x32-10 blocks of the workload (>= 36 lane-
-    # instructions per block) at the SMs' issue peak (4 warp-instr/clk/SM).
-    dpb = 2 if stream == pb.STREAM_U53 else 4
+    # Ceiling the injected stream imposes: a kernel doing
+    # nothing but generating the workload's Philox4x32-10 blocks, at the
+    # measured Philox-only rate of a B200.
+    dpb = 4  # both streams: 4 high words per Philox block (U53 low words only on ties)
     n_alias = int(np.count_nonzero(flat.grp_alias_size))
     has_leaf = 1 if a.method != "old" else 0
     blocks = (-(-(flat.pert_groups + has_leaf) // dpb)) * traj_steps + (-(-n_alias // dpb)) * fn_total
-    issue_peak = props.multi_processor_count * 4 * sm_mhz * 1e6
-    rng_ceiling_steps = issue_peak / (blocks * 36 / 32 / traj_steps)
+    # measured: the engine's own Philox4x32-10 issues at most this many blocks
+    # per second on a B200 (tools/ceilings.cu, profiles/r02_ceilings.jsonl)
+    philox_peak_blocks = PHILOX_BLOCKS_PER_S
+    rng_ceiling_steps = philox_peak_blocks / (blocks / traj_steps)
     rng_ceiling = rng_ceiling_steps * lookups / traj_steps
     info = eng.info()
     spill = None
@@ -610,9 +617,9 @@ def run_ours(a):
                      "lookups_per_step": lookups / traj_steps,
                      "rng_ceiling_frac": rng_ceiling / peak_lookups,
                      "frac_of_rng_ceiling": achieved / rng_ceiling,
-                     "rng_ceiling_note": "lookup rate of a kernel issuing only the workload's "
-                                         "Philox4x32-10 blocks (36 lane-instr each) at the issue "
-                                         "peak; DESIGN.md section 7"},
+                     "rng_ceiling_note": "lookup rate of a kernel generating only the workload's "
+                                         "Philox4x32-10 blocks at the measured Philox-only rate "
+                                         "of a B200 (profiles/r02_ceilings.jsonl); DESIGN.md §7"},
         "clocks": clk.summary(),
     }
     if not a.no_cpu_baseline and world == 1:

@@ -238,6 +238,16 @@ int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states,
 int pbn_philox_kat(const uint32_t* ctr, uint32_t n, uint64_t seed, uint32_t* out);
 /* Launch count of the last run call (kernels launched). */
 uint32_t pbn_gpu_last_launches(const pbn_gpu* g);
+/* The kernel the last run launched, e.g.
+ * "subwarp<lpt=32,gather=shfl_compact,stream=u53,place=tables,warps=28>" or
+ * "lane<scan,stream=u53,place=all,warps=28>" (NUL-terminated into buf[cap];
+ * *len_out = full length). */
+int pbn_gpu_last_kernel(const pbn_gpu* g, char* buf, size_t cap, size_t* len_out);
+/* The kernel a run of n_traj trajectories with `flags` would launch (same
+ * format), without running: lets a test pin that it exercised the very
+ * instantiation a benchmark of another ensemble size runs. */
+int pbn_gpu_plan_launch(const pbn_gpu* g, uint32_t n_traj, uint32_t stream, uint32_t flags,
+                        char* buf, size_t cap, size_t* len_out);
 void pbn_gpu_destroy(pbn_gpu* g);
 
 /* ---- pooled ensemble steady-state estimate (estimator.hpp:137-244) ---------- */

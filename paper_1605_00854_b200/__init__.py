@@ -175,6 +175,9 @@ def _load():
                             C.POINTER(U64)]),
         "pbn_gpu_run_device": (I, [P, C.POINTER(RunArgs), P, P, P, P]),
         "pbn_gpu_last_launches": (U32, [P]),
+        "pbn_gpu_last_kernel": (I, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "pbn_gpu_plan_launch": (I, [P, U32, U32, U32, C.c_char_p, C.c_size_t,
+                                    C.POINTER(C.c_size_t)]),
         "pbn_gpu_destroy": (None, [P]),
         "pbn_philox_kat": (I, [C.POINTER(U32), U32, U64, C.POINTER(U32)]),
         "pbn_estimate": (I, [P, C.POINTER(EstimateRequest), C.POINTER(U32), C.POINTER(C.c_uint8),
@@ -206,7 +209,8 @@ EXPORTED_SYMBOLS = (
     "pbn_model_free", "pbn_prepare", "pbn_prepare_nodewise",
     "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
     "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
-    "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_destroy", "pbn_estimate",
+    "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_last_kernel", "pbn_gpu_plan_launch",
+    "pbn_gpu_destroy", "pbn_estimate",
     "pbn_estimate_with_backend", "pbn_series_stats_host", "pbn_inverse_normal_cdf",
     "pbn_series_stats_device",
 )
@@ -513,7 +517,7 @@ class GpuEnsemble:
                                 C.byref(wpc)))
         return {"lanes_per_traj": lpt.value, "placement": ("global", "core", "tables", "all", "core_pert")[place.value],
                 "staged_smem_bytes": sm.value, "plan_bytes": pb.value,
-                "warps_per_cta": wpc.value}
+                "warps_per_cta": wpc.value, "kernel": self.last_kernel()}
 
     def _args(self, seed, traj_begin, n_traj, n_steps, step_begin, pred, stream):
         a = RunArgs()
@@ -589,6 +593,19 @@ class GpuEnsemble:
 
     def last_launches(self) -> int:
         return int(lib.pbn_gpu_last_launches(self._h))
+
+    def last_kernel(self) -> str:
+        """The kernel instantiation the last run launched (pbn_gpu_last_kernel)."""
+        buf = C.create_string_buffer(256)
+        _check(lib.pbn_gpu_last_kernel(self._h, buf, 256, None))
+        return buf.value.decode()
+
+    def plan_launch(self, n_traj: int, stream: int = STREAM_U53, node_counts: bool = False) -> str:
+        """The kernel a run of n_traj trajectories would launch (pbn_gpu_plan_launch)."""
+        buf = C.create_string_buffer(256)
+        _check(lib.pbn_gpu_plan_launch(self._h, n_traj, stream,
+                                       RUN_NODE_COUNTS if node_counts else 0, buf, 256, None))
+        return buf.value.decode()
 
 
 # ----------------------------------------------------------------------------

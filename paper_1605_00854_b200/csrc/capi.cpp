@@ -32,6 +32,7 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
                                  std::uint64_t* d_counts, cudaStream_t stream,
                                  std::uint32_t* launches);
 bool lane_kernel_fits(const dev_plan_header& h);
+int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt);
 std::uint32_t lane_max_warps();
 std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
@@ -72,6 +73,7 @@ struct pbn_gpu {
   std::uint32_t lpt_fixed = 0;  // 0: chosen per run
   std::uint32_t last_lpt = 0;
   int last_place = -1;  // placement the last launch actually ran (-1: none yet)
+  std::string last_kernel;  // kernel_name() of the last launch
   // device workspace kept across calls: pbn_estimate's states, counts,
   // carried samples, two pilot-series buffers and reduction scratch (0-5);
   // pbn_gpu_run's carried samples, series and node counts (6-8)
@@ -123,11 +125,6 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // Lane kernel: scan phase A ahead per lane when fewer steps than this reach
 // the function phase (c1: 0.37 -> +22%; c3: 0.91 -> -17%).
 constexpr double kScanBelow = 0.65;
-// Word-per-block phase A above this per-group flip probability.
-#ifndef PBN_WORDS_ABOVE
-#define PBN_WORDS_ABOVE 0.01
-#endif
-constexpr double kWordsAbove = PBN_WORDS_ABOVE;
 
 // Probability that a step reaches the function phase: no kept node flips
 // (every pattern draw returns 0, or every Bernoulli draw misses) and the leaf
@@ -272,29 +269,24 @@ dev_run_params make_params(const pbn_gpu& g, const pbn_run_args& a) {
   return rp;
 }
 
-void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
-                std::uint64_t* d_counts, std::uint64_t* d_node_counts, cudaStream_t stream) {
-  dev_run_params rp = make_params(g, a);
-  if (a.n_traj == 0) return;
-  const bool nc = (a.flags & PBN_RUN_NODE_COUNTS) != 0;
-  if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
-  rp.node_counts = nc ? d_node_counts : nullptr;
-  // word-per-block phase A (U53): pays when groups flip often or a lane owns
-  // several phase-A blocks (c5: +2..11 % over p = 1e-4..0.1; c2, one block per
-  // lane and 1.6 % of groups flipping: +0.2 %)
-  {
-    const std::uint32_t lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
-    const std::uint32_t blocks53 = (g.ep.h.g + g.ep.h.has_leaf + 1) / 2;
-    rp.phase_a_words = (g.p_group_flip > kWordsAbove || blocks53 > lpt) ? 1u : 0u;
-  }
-  ck(cudaSetDevice(g.device), "cudaSetDevice");
-  g.last_lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, a.n_traj, g.sms);
-  // the counter planes take shared memory: fall back to a leaner plan
-  // placement if the ensemble no longer fits next to the staged plan
+// What a run of n_traj trajectories launches: kernel, lanes per trajectory,
+// warps per CTA, plan placement (possibly stepped down from the configured
+// one when the ensemble's per-trajectory state does not fit next to it).
+struct launch_choice {
+  std::uint32_t lpt = 0, warps = 0;
+  int place = 0;
+  bool lane = false, scan = false;
+  int gm = 0;
+};
+
+launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc) {
+  pbn_gpu& g = const_cast<pbn_gpu&>(g0);  // pick_warps reads g.place; restored below
+  launch_choice c;
+  c.lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, n_traj, g.sms);
   const int place0 = g.place;
   for (;;) {
     try {
-      g.last_warps = pick_warps(g, a.n_traj, g.last_lpt, nc);
+      c.warps = pick_warps(g, n_traj, c.lpt, nc);
       break;
     } catch (const resource_error&) {
       if (g.place == 0) {
@@ -304,15 +296,43 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
       g.place = next_lower_place(g.place);
     }
   }
+  c.place = g.place;
+  g.place = place0;
+  c.lane = c.lpt == 1 && lane_kernel_fits(g.ep.h);
+  c.scan = c.lane && g.p_fn < kScanBelow;
+  c.gm = c.lane ? -1 : ensemble_gather_mode(g.ep.h, c.lpt);
+  return c;
+}
+
+std::string kernel_name(const launch_choice& c, std::uint32_t stream) {
+  static const char* places[] = {"global", "core", "tables", "all", "core_pert"};
+  static const char* gms[] = {"smem", "shfl", "shfl_compact", "shfl2"};
+  std::string s = c.lane ? std::string("lane<") + (c.scan ? "scan" : "lockstep")
+                         : "subwarp<lpt=" + std::to_string(c.lpt) + ",gather=" + gms[c.gm];
+  s += std::string(",stream=") + (stream == PBN_STREAM_U53 ? "u53" : "u32");
+  s += std::string(",place=") + places[c.place] + ",warps=" + std::to_string(c.warps) + ">";
+  return s;
+}
+
+void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
+                std::uint64_t* d_counts, std::uint64_t* d_node_counts, cudaStream_t stream) {
+  dev_run_params rp = make_params(g, a);
+  if (a.n_traj == 0) return;
+  const bool nc = (a.flags & PBN_RUN_NODE_COUNTS) != 0;
+  if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
+  rp.node_counts = nc ? d_node_counts : nullptr;
+  ck(cudaSetDevice(g.device), "cudaSetDevice");
+  const launch_choice c = choose_launch(g, a.n_traj, nc);
+  g.last_lpt = c.lpt;
+  g.last_warps = c.warps;
+  g.last_place = c.place;
+  g.last_kernel = kernel_name(c, a.stream);
   g.launches = 0;
   const cudaError_t e =
-      g.last_lpt == 1 && lane_kernel_fits(g.ep.h)
-          ? launch_lane_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream),
-                                 g.p_fn < kScanBelow, g.last_warps, rp, d_states, d_counts, stream, &g.launches)
-          : launch_ensemble(g.ep.h, g.d_blob, g.place, static_cast<int>(a.stream), g.last_lpt,
-                            g.last_warps, rp, d_states, d_counts, stream, &g.launches);
-  g.last_place = g.place;
-  g.place = place0;
+      c.lane ? launch_lane_ensemble(g.ep.h, g.d_blob, c.place, static_cast<int>(a.stream), c.scan,
+                                    c.warps, rp, d_states, d_counts, stream, &g.launches)
+             : launch_ensemble(g.ep.h, g.d_blob, c.place, static_cast<int>(a.stream), c.lpt,
+                               c.warps, rp, d_states, d_counts, stream, &g.launches);
   ck(e, "ensemble launch");
 }
 
@@ -669,6 +689,31 @@ int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states, ui
 }
 
 uint32_t pbn_gpu_last_launches(const pbn_gpu* g) { return g ? g->launches : 0; }
+
+static void copy_str(const std::string& s, char* buf, size_t cap, size_t* len_out) {
+  if (len_out) *len_out = s.size();
+  if (buf && cap) {
+    const std::size_t k = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+}
+
+int pbn_gpu_last_kernel(const pbn_gpu* g, char* buf, size_t cap, size_t* len_out) {
+  return guard([&] {
+    need(g, "gpu");
+    copy_str(g->last_kernel, buf, cap, len_out);
+  });
+}
+
+int pbn_gpu_plan_launch(const pbn_gpu* g, uint32_t n_traj, uint32_t stream, uint32_t flags,
+                        char* buf, size_t cap, size_t* len_out) {
+  return guard([&] {
+    need(g, "gpu");
+    const launch_choice c = choose_launch(*g, n_traj, (flags & PBN_RUN_NODE_COUNTS) != 0);
+    copy_str(kernel_name(c, stream), buf, cap, len_out);
+  });
+}
 
 void pbn_gpu_destroy(pbn_gpu* g) {
   if (!g) return;

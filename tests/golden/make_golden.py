@@ -24,12 +24,21 @@ import oracle  # noqa: E402
 from helpers import config_text, flat_of, plan_digest  # noqa: E402
 
 FIXTURES = {
-    # name: (config, k_max, mgp, n_traj, n_steps)
-    "c1": ("c1", 12, 8, 8, 600),
-    "c2": ("c2", 12, 8, 4, 200),
-    "c3": ("c3", 12, 8, 8, 600),
-    "c4": ("c4", 12, 12, 2, 60),
-    "c5": ("c5", 12, 8, 4, 200),
+    # name: (config, k_max, mgp, n_traj, n_steps, p override)
+    # the benchmarked plans (bench.py / workloads.json: theta 2^25, k 16,
+    # mgp 8; c4 mgp 12) and the c5 sweep's perturbation rates
+    "c1_bench": ("c1", 16, 8, 8, 600, None),
+    "c2_bench": ("c2", 16, 8, 6, 300, None),
+    "c3_bench": ("c3", 16, 8, 8, 600, None),
+    "c4_bench": ("c4", 16, 12, 2, 60, None),
+    "c5_bench": ("c5", 16, 8, 4, 200, None),
+    "c5_p0.1": ("c5", 16, 8, 4, 200, 0.1),
+    "c5_p0.001": ("c5", 16, 8, 4, 200, 0.001),
+    "c5_p0.0001": ("c5", 16, 8, 4, 200, 0.0001),
+    # the reference's default plan (engine.hpp:81-83) and a k = 12 plan
+    "c2_ref_default": ("c2", 16, 18, 4, 200, None),
+    "c1_k12": ("c1", 12, 8, 8, 600, None),
+    "c2_k12": ("c2", 12, 8, 4, 200, None),
 }
 SEED, TRAJ_BEGIN, STEP_BEGIN = 42, 1000, 7
 
@@ -37,8 +46,8 @@ SEED, TRAJ_BEGIN, STEP_BEGIN = 42, 1000, 7
 def main():
     ref = oracle.Reference()
     manifest = {}
-    for name, (cfg, k, mgp, n_traj, n_steps) in FIXTURES.items():
-        text, terms = config_text(cfg)
+    for name, (cfg, k, mgp, n_traj, n_steps, p) in FIXTURES.items():
+        text, terms = config_text(cfg, p)
         rplan = ref.parse(text).prepare(1 << 25, k, mgp)
         pred = rplan.compile_predicate(terms)
         out = {}
@@ -50,7 +59,7 @@ def main():
         out["pred_bits"], out["pred_vals"] = pred
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
         manifest[name] = {
-            "config": cfg, "k_max": k, "mgp": mgp, "theta": 1 << 25, "n_traj": n_traj,
+            "config": cfg, "p": p, "k_max": k, "mgp": mgp, "theta": 1 << 25, "n_traj": n_traj,
             "n_steps": n_steps, "seed": SEED, "traj_begin": TRAJ_BEGIN, "step_begin": STEP_BEGIN,
             "model_sha256": hashlib.sha256(text.encode()).hexdigest(),
             "plan_digest": plan_digest(flat_of(rplan.view)), "n_kept": rplan.n_kept,
@@ -69,9 +78,9 @@ def steady_state_reference():
     pooled device estimate at r = 1e-3 is compared against."""
     ref = oracle.Reference()
     text, terms = config_text("c3")
-    rplan = ref.parse(text).prepare(1 << 25, 12, 8)
+    rplan = ref.parse(text).prepare(1 << 25, 16, 8)
     est = rplan.estimate(terms, 2.5e-4, 0.95, 10000, 2024, -1, 0)
-    out = {"config": "c3", "k_max": 12, "mgp": 8, "precision": 2.5e-4, "confidence": 0.95,
+    out = {"config": "c3", "k_max": 16, "mgp": 8, "precision": 2.5e-4, "confidence": 0.95,
            "seed": 2024, "terms": terms, **est}
     with open(os.path.join(HERE, "c3_steady_state.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)

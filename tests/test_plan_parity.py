@@ -9,8 +9,9 @@ from helpers import config_text, flat_of, plan_diff
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
-@pytest.mark.parametrize("k,mgp", [(12, 8), (16, 12), (8, 6)])
+@pytest.mark.parametrize("k,mgp", [(16, 8), (16, 18), (12, 8), (16, 12), (8, 6)])
 def test_baseline_configs_identical(pb, ref, name, k, mgp):
+    """(16, 8) is every bench plan but c4's; (16, 18) the reference default."""
     text, terms = config_text(name)
     mine = pb.prepare(pb.parse_model(text), 1 << 25, k, mgp)
     theirs = ref.parse(text).prepare(1 << 25, k, mgp)
@@ -83,3 +84,12 @@ def test_serialization_identical(pb, ref):
     for name in ["c1", "c3"]:
         text, _ = config_text(name)
         assert pb.parse_model(text).serialize() == ref.parse(text).serialize()
+
+
+@pytest.mark.slow
+def test_c4_bench_plan_identical(pb, ref):
+    """c4's bench plan (k 16, mgp 12): the spill workload."""
+    text, _ = config_text("c4")
+    mine = pb.prepare(pb.parse_model(text), 1 << 25, 16, 12)
+    theirs = ref.parse(text).prepare(1 << 25, 16, 12)
+    assert plan_diff(mine.flat(), flat_of(theirs.view)) == []
