@@ -514,6 +514,21 @@ def run_ours(a):
                                      C.cast(host_states.data_ptr(), C.POINTER(C.c_uint64)),
                                      C.cast(host_counts.data_ptr(), C.POINTER(C.c_uint64)), None))
 
+    grp = None
+    if world > 1:
+        # N > 1: end to end through the C-ABI device group (pbn_group_run):
+        # host rows in, this rank's launch, pooling kernels, ONE ncclAllReduce
+        # of the pooled counts, host rows + job totals out
+        ids = [pb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        grp = pb.GpuGroup(plan, device=local, nranks=world, rank=rank, nccl_id=ids[0])
+        g_states = np.zeros((n_traj, words), np.uint64)
+
+        def e2e_one(n_steps, s0):  # noqa: F811
+            nonlocal g_states
+            g_states, _, _, _ = grp.simulate(42, n_traj * world, n_steps, step_begin=s0,
+                                             states=g_states, pred=pred, stream=stream)
+
     e2e_one(max(1, sim_steps // 10), 0)
     if world > 1:
         dist.barrier()
@@ -525,6 +540,7 @@ def run_ours(a):
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_val = traj_steps * flat.n_kept / float(e2e_t.item())
+    info = eng.info()  # the timed kernel (before the alternate-stream run below)
 
     if rank != 0:
         if world > 1:
@@ -565,7 +581,7 @@ def run_ours(a):
     # Ceiling the injected stream imposes: a kernel doing
     # nothing but generating the workload's Philox4x32-10 blocks, at the
     # measured Philox-only rate of a B200.
-    dpb = 4  # both streams: 4 high words per Philox block (U53 low words only on ties)
+    dpb = 2 if stream == pb.STREAM_U53 else 4
     n_alias = int(np.count_nonzero(flat.grp_alias_size))
     has_leaf = 1 if a.method != "old" else 0
     blocks = (-(-(flat.pert_groups + has_leaf) // dpb)) * traj_steps + (-(-n_alias // dpb)) * fn_total
@@ -574,7 +590,6 @@ def run_ours(a):
     philox_peak_blocks = PHILOX_BLOCKS_PER_S
     rng_ceiling_steps = philox_peak_blocks / (blocks / traj_steps)
     rng_ceiling = rng_ceiling_steps * lookups / traj_steps
-    info = eng.info()
     spill = None
     if info["placement"] == "global":
         # spill case: the plan is read through L1/L2. The lookup
@@ -601,6 +616,8 @@ def run_ours(a):
         "node_updates_per_s_original_n": traj_steps * w.n / (total_ms / 1e3),
         "fn_phase_fraction": fn_total / traj_steps,
         "e2e": {"value": e2e_val, "unit": UNIT,
+                "path": ("pbn_group_run (C-ABI device group: one ncclAllReduce of the pooled "
+                         "counts)" if world > 1 else "pbn_gpu_run (C-ABI, host buffers)"),
                 "h2d_bytes_per_step": n_traj * words * 8,
                 "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
         "gpu_launches": launches,
@@ -639,11 +656,35 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def launch_ranks(a):
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks (one process per GPU) through torch.distributed.run, the way the
+    driver launches it. Under torchrun, WORLD_SIZE must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != a.gpus:
+            sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {a.gpus}")
+        return False
+    if a.gpus <= 1:
+        return False
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     a = parse()
     if a.impl == "reference":
-        run_reference_arm(a)
+        run_reference_arm(a)  # rank 0 alone (other ranks exit without work)
     else:
+        launch_ranks(a)
         run_ours(a)
 
 

@@ -250,6 +250,43 @@ int pbn_gpu_plan_launch(const pbn_gpu* g, uint32_t n_traj, uint32_t stream, uint
                         char* buf, size_t cap, size_t* len_out);
 void pbn_gpu_destroy(pbn_gpu* g);
 
+/* ---- device group: one ensemble over several GPUs ----------
+ * The job's trajectories (global ids a->traj_begin .. + a->n_traj) are split
+ * into contiguous per-rank ranges, one rank per device (rank r gets
+ * n/R + (r < n%R) ids starting at r*(n/R) + min(r, n%R)); the plan is
+ * replicated; the only collective is ONE ncclAllReduce (sum) of the pooled
+ * counts (+ the pooled per-node one-counts with PBN_RUN_NODE_COUNTS) over
+ * NVLink. Draws are keyed by global trajectory id, so every result is
+ * identical for any device count. NCCL is bound at run time (libnccl.so.2);
+ * without it the create calls return PBN_ERESOURCE.
+ * Replaces: a caller looping simulate() (engine.hpp:371-384) over independent
+ * trajectories and summing the results (pbn_main.cpp:230-240 runs one). */
+typedef struct pbn_group pbn_group;
+/* One process drives every device: devices[n_devices] (NULL: 0..n-1), ncclCommInitAll. */
+int pbn_group_create(const pbn_plan_view* view, const int* devices, uint32_t n_devices,
+                     uint32_t lanes_per_traj, pbn_group** out);
+/* One process per device: rank `rank` of `nranks`; nccl_id = 128 bytes from
+ * pbn_nccl_unique_id() on one rank, shared by the caller (MPI, a file, ...). */
+int pbn_nccl_unique_id(uint8_t* nccl_id_out);
+int pbn_group_create_rank(const pbn_plan_view* view, int device, uint32_t nranks, uint32_t rank,
+                          const uint8_t* nccl_id, uint32_t lanes_per_traj, pbn_group** out);
+int pbn_group_info(const pbn_group* gr, uint32_t* n_members, uint32_t* nranks,
+                   uint32_t* first_rank);
+/* The id range of rank `rank` for a job of n_total trajectories. */
+int pbn_group_shard(const pbn_group* gr, uint64_t n_total, uint32_t rank, uint64_t* begin,
+                    uint64_t* count);
+/* Member i's engine (owned by the group), e.g. for pbn_gpu_info / last_kernel. */
+int pbn_group_member(const pbn_group* gr, uint32_t i, pbn_gpu** eng);
+/* Runs the whole job (collective: every rank calls it with the same args).
+ * states_inout / counts_out (NULL allowed) hold THIS process's rows only —
+ * the trajectories of its ranks, in global id order, row 0 = its first rank's
+ * first trajectory. totals_out[PBN_COUNT_FIELDS] = job-wide pooled counts;
+ * node_totals_out[n_kept] (iff PBN_RUN_NODE_COUNTS) = job-wide pooled
+ * one-counts. No series / tprev (PBN_EUSAGE). Synchronous. */
+int pbn_group_run(pbn_group* gr, const pbn_run_args* a, uint64_t* states_inout,
+                  uint64_t* counts_out, uint64_t* totals_out, uint64_t* node_totals_out);
+void pbn_group_destroy(pbn_group* gr);
+
 /* ---- pooled ensemble steady-state estimate (estimator.hpp:137-244) ---------- */
 typedef struct pbn_estimate_request {
   double precision;          /* r       (estimator.hpp:60) */

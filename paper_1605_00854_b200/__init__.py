@@ -187,6 +187,16 @@ def _load():
         "pbn_series_stats_host": (I, [C.POINTER(U32), U32, U64, U64, U32, C.POINTER(U64)]),
         "pbn_inverse_normal_cdf": (C.c_double, [C.c_double]),
         "pbn_series_stats_device": (I, [I, P, U32, U64, U64, U32, C.POINTER(U64)]),
+        "pbn_group_create": (I, [C.POINTER(PlanView), C.POINTER(I), U32, U32, C.POINTER(P)]),
+        "pbn_nccl_unique_id": (I, [C.POINTER(C.c_uint8)]),
+        "pbn_group_create_rank": (I, [C.POINTER(PlanView), I, U32, U32, C.POINTER(C.c_uint8), U32,
+                                      C.POINTER(P)]),
+        "pbn_group_info": (I, [P, C.POINTER(U32), C.POINTER(U32), C.POINTER(U32)]),
+        "pbn_group_shard": (I, [P, U64, U32, C.POINTER(U64), C.POINTER(U64)]),
+        "pbn_group_member": (I, [P, U32, C.POINTER(P)]),
+        "pbn_group_run": (I, [P, C.POINTER(RunArgs), C.POINTER(U64), C.POINTER(U64),
+                              C.POINTER(U64), C.POINTER(U64)]),
+        "pbn_group_destroy": (None, [P]),
         "pbn_internal_lower_bound": (U32, [C.POINTER(U32), U32, U64]),
         "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
         "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
@@ -212,7 +222,8 @@ EXPORTED_SYMBOLS = (
     "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_last_kernel", "pbn_gpu_plan_launch",
     "pbn_gpu_destroy", "pbn_estimate",
     "pbn_estimate_with_backend", "pbn_series_stats_host", "pbn_inverse_normal_cdf",
-    "pbn_series_stats_device",
+    "pbn_series_stats_device", "pbn_group_create", "pbn_nccl_unique_id", "pbn_group_create_rank",
+    "pbn_group_info", "pbn_group_shard", "pbn_group_member", "pbn_group_run", "pbn_group_destroy",
 )
 
 
@@ -606,6 +617,86 @@ class GpuEnsemble:
         _check(lib.pbn_gpu_plan_launch(self._h, n_traj, stream,
                                        RUN_NODE_COUNTS if node_counts else 0, buf, 256, None))
         return buf.value.decode()
+
+
+class GpuGroup:
+    """One ensemble over several GPUs through the C-ABI device group
+    (pbn_group_*): contiguous per-rank trajectory ranges, the plan
+    replicated, ONE ncclAllReduce of the pooled counts (+ per-node one-counts).
+
+    GpuGroup(plan, devices=[0, 1, ...])            one process, every device
+    GpuGroup(plan, device=d, nranks=R, rank=r, nccl_id=id)   one process per device
+    (nccl_id: 128 bytes from nccl_unique_id() on one rank, shared by the caller)."""
+
+    def __init__(self, plan, devices=None, lanes_per_traj=0, device=None, nranks=None,
+                 rank=None, nccl_id=None):
+        view = plan.view if isinstance(plan, PreparedSimulation) else plan
+        self._keep = plan
+        self.n_kept = view.n_kept
+        self.words = state_words(self.n_kept)
+        h = C.c_void_p()
+        if nranks is None:
+            devs = list(range(device_count())) if devices is None else list(devices)
+            arr = (C.c_int * len(devs))(*devs)
+            _check(lib.pbn_group_create(C.byref(view), arr, len(devs), lanes_per_traj, C.byref(h)))
+        else:
+            idb = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            _check(lib.pbn_group_create_rank(C.byref(view), device, nranks, rank, idb,
+                                             lanes_per_traj, C.byref(h)))
+        self._h = h
+        n, r, f = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib.pbn_group_info(h, C.byref(n), C.byref(r), C.byref(f)))
+        self.n_members, self.nranks, self.first_rank = n.value, r.value, f.value
+
+    def __del__(self):
+        if lib is not None and getattr(self, "_h", None) and self._h.value:
+            lib.pbn_group_destroy(self._h)
+            self._h = C.c_void_p(None)
+
+    def shard(self, n_total: int, rank: int):
+        b, c = C.c_uint64(), C.c_uint64()
+        _check(lib.pbn_group_shard(self._h, n_total, rank, C.byref(b), C.byref(c)))
+        return b.value, c.value
+
+    def local_rows(self, n_total: int):
+        """[begin, end) of the global rows this process's members own."""
+        b0, _ = self.shard(n_total, self.first_rank)
+        bl, cl = self.shard(n_total, self.first_rank + self.n_members - 1)
+        return b0, bl + cl
+
+    def member_kernel(self, i: int = 0) -> str:
+        eng = C.c_void_p()
+        _check(lib.pbn_group_member(self._h, i, C.byref(eng)))
+        buf = C.create_string_buffer(256)
+        _check(lib.pbn_gpu_last_kernel(eng, buf, 256, None))
+        return buf.value.decode()
+
+    def simulate(self, seed, n_traj, n_steps, traj_begin=0, step_begin=0, states=None, pred=None,
+                 stream=STREAM_U53, node_counts=False):
+        """The whole job of n_traj trajectories (collective over the ranks).
+        states: this process's rows (local_rows) or None (zeros).
+        Returns (states, per-trajectory counts, job totals (8,), job node totals or None)."""
+        b, e = self.local_rows(n_traj)
+        rows = e - b
+        st = (np.zeros((rows, self.words), np.uint64) if states is None
+              else np.ascontiguousarray(states, np.uint64).copy())
+        if st.shape != (rows, self.words):
+            raise UsageError(f"states must be ({rows}, {self.words}) for this process's rows")
+        cnt = np.zeros((rows, COUNT_FIELDS), np.uint64)
+        tot = np.zeros(COUNT_FIELDS, np.uint64)
+        ntot = np.zeros(self.n_kept, np.uint64) if node_counts else None
+        a = GpuEnsemble._args(self, seed, traj_begin, n_traj, n_steps, step_begin, pred, stream)
+        a.flags = RUN_NODE_COUNTS if node_counts else 0
+        _check(lib.pbn_group_run(self._h, C.byref(a), _u64p(st), _u64p(cnt), _u64p(tot),
+                                 _u64p(ntot) if node_counts else None))
+        return st, cnt, tot, ntot
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for GpuGroup(..., nranks=R, rank=r, nccl_id=id)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib.pbn_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 # ----------------------------------------------------------------------------

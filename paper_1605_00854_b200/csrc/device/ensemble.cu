@@ -52,8 +52,8 @@ constexpr int kMaxWarpsLpt32 = 28;
 // (general groups gather from shared memory: they run under divergence).
 template <int LPT, int STREAM, int PLACE, int GM>
 __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
-    pbn_ensemble_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
-                        const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
+    pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
+                        const dev_run_params rp, std::uint64_t* __restrict__ states,
                         std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool RG = GM >= 1;
   constexpr bool RG2 = GM == 3;
   constexpr bool SC = GM == 2;
+  // U53 compact kernels keep only the draws' high words in the chunk buffer
+  // (c2 +2.4 %; the general-path kernels lose 2-5 % to the recompute path)
+  constexpr bool HI = STREAM == STREAM_U53 && SC;
 
   const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   auto alias_fast = [&](const uint4* cells, std::uint32_t asz, std::uint32_t ab,
                         std::uint32_t jj, bool& rare) -> std::uint32_t {
     if constexpr (STREAM == STREAM_U53) {
-      const std::uint32_t hi = dbuf[jj];  // the draw's high word: bits [21, 53) of r53
+      const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
       const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
       const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + e));  // {alias, hi32(C)}
@@ -195,10 +198,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
   // contraction, exactly as engine.hpp:285-290 computes it (U53 only).
   auto alias_exact = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
-    // the chunk holds the draws' high words; the low word is word d % DPB of
-    // the draw's low block (philox.cuh kLoBlock)
-    const std::uint32_t d = jbase + jj;  // draw index within the alias region
-    const raw53 rw{dbuf[jj], lo_word<STREAM>(sp, nb0 + d / DPB, d % DPB, rp.rk0, rp.rk1)};
+    raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
+    if constexpr (HI) {  // the chunk keeps only the draws' high words: recompute the block
+      const std::uint32_t d = jbase + jj;  // draw index within the alias region
+      rw = pick53(philox_block(sp, nb0 + d / DPB, rp.rk0, rp.rk1), d % DPB);
+    }
     const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
     const double xx = __dmul_rn(u, __uint2double_rn(asz));
     std::uint32_t c = __double2uint_rz(xx);
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       const uint4 ar = ldp<GC>(arec4 + j);  // {U53 cell offset, function offset, N, ~N}
       std::uint32_t pick;
       if constexpr (STREAM == STREAM_U53) {
-        const std::uint32_t hi = dbuf[jj];
+        const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];
         const std::uint64_t P = static_cast<std::uint64_t>(hi) * ar.z;
         const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
         const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 8 * kScolSlots * e));
@@ -493,69 +497,38 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     // before the last group, the k'-bit mask for the last group (engine.hpp:
     // 261) and nothing for the leaf draw and the block's unused tail.
     bool flip = false, leaf = false;
-    // One Philox block of phase A: draws b*DPB .. b*DPB+DPB-1. Every draw is
-    // looked up; a per-draw mask keeps full patterns for draws before the
-    // last group, the k'-bit mask for the last group (engine.hpp:261) and
-    // nothing for the leaf draw and the block's unused tail. U53: decided on
-    // the high words; a tie recomputes the block's decisions with the low
-    // words (one more Philox block, ~2^-14 of blocks at k = 16).
-    // WORDS (k * DPB a multiple of 32, k = 8/16/24): the block's patterns fill
-    // exactly state words b*WPB.., which no other lane touches — they are
-    // OR-ed together and XOR-ed in with plain read-modify-writes instead of
-    // per-draw shared atomics.
-    const bool words = (k * DPB) % 32 == 0;
-    const std::uint32_t wpb = k * DPB / 32;
+    // one Philox block of phase A: draws b*DPB .. b*DPB+DPB-1
     auto phase_a_block = [&](std::uint32_t b, auto bern_c) {
       constexpr bool BERN = decltype(bern_c)::value;  // Method_old / Method_reduction plans
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
       const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
-      std::uint32_t c[DPB];
-      bool rare = false, lf = false;
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e) {
-        c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), false, 0u, rare);
-        if (static_cast<int>(e) == rem && h.has_leaf) lf = pa_leaf<STREAM>(h, pick32(x, e), false, 0u, rare);
-      }
-      if constexpr (STREAM == STREAM_U53) {
-        if (__builtin_expect(rare, 0)) {
-          const uint4 y = philox_lo_block(sp, b, rp.rk0, rp.rk1);
-          bool unused = false;
-#pragma unroll
-          for (std::uint32_t e = 0; e < DPB; ++e) {
-            c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), true, pick32(y, e), unused);
-            if (static_cast<int>(e) == rem && h.has_leaf)
-              lf = pa_leaf<STREAM>(h, pick32(x, e), true, pick32(y, e), unused);
-          }
+        std::uint32_t c;
+        if constexpr (BERN) {  // per-node flip iff u < p (engine.hpp:198)
+          if constexpr (STREAM == STREAM_U53)
+            c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
+          else
+            c = pick32(x, e) < h.pthr32 ? 1u : 0u;
+        } else if constexpr (STREAM == STREAM_U53) {
+          c = pert_draw53<GP>(pert53, pick53(x, e), k);
+        } else {
+          c = pert_draw32<GP>(pert32, pick32(x, e), k);
         }
-      }
-      if (lf) leaf = true;
-      std::uint64_t w01 = 0;  // the block's words 0, 1 (WORDS)
-      std::uint32_t w2 = 0;   // word 2 (k = 24)
-#pragma unroll
-      for (std::uint32_t e = 0; e < DPB; ++e) {
         const int q = rem - 1 - static_cast<int>(e);
-        const std::uint32_t ce = c[e] & (q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u));
-        if (!BERN && words) {
-          const std::uint32_t o = e * k;  // bit offset within the block's words
-          if (o < 64) {
-            w01 |= static_cast<std::uint64_t>(ce) << o;
-            if (o + k > 64) w2 |= ce >> (64 - o);
-          } else {
-            w2 |= ce << (o - 64);
-          }
-        } else if (__builtin_expect(ce != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+        c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+        if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
           flip = true;
           const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
-          atomicXor(Sc + w, ce << sh);
-          if (sh != 0 && (ce >> (32 - sh)) != 0) atomicXor(Sc + w + 1, ce >> (32 - sh));
+          atomicXor(Sc + w, c << sh);
+          if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
         }
-      }
-      if (!BERN && words && __builtin_expect((w01 | w2) != 0, 0)) {
-        flip = true;
-        const std::uint32_t w0 = static_cast<std::uint32_t>(w01), w1 = static_cast<std::uint32_t>(w01 >> 32);
-        if (w0) Sc[b * wpb] ^= w0;
-        if (w1) Sc[b * wpb + 1] ^= w1;  // zero unless wpb >= 2
-        if (w2) Sc[b * wpb + 2] ^= w2;  // zero unless wpb == 3
+        if (q == -1 && h.has_leaf) {  // this element is the leaf draw (engine.hpp:268)
+          if constexpr (STREAM == STREAM_U53)
+            leaf = pick53(x, e).raw() > h.leaf_thr53;
+          else
+            leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
+        }
       }
     };
     auto phase_a = [&](auto bern_c) {
@@ -565,8 +538,48 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t b = r; b < nb0; b += LPT) phase_a_block(b, bern_c);
       }
     };
+    // k * DPB == 32 (U53 with k = 16, U32 with k = 8): block b's patterns
+    // fill exactly state word b, which no other lane touches — the patterns
+    // are OR-ed into one word and XOR-ed in with a plain read-modify-write
+    // instead of per-draw atomics (c5 at p = 0.1 flips ~3 groups per lane and
+    // step). Masks only matter in the block of the last group / leaf draw.
+    auto phase_a_words = [&]() {
+      if constexpr (STREAM != STREAM_U53) return;  // U53 only (U32 kernels keep their code)
+      constexpr std::uint32_t K = 32 / DPB;
+      for (std::uint32_t b = r; b < nb0; b += LPT) {
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+        const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
+        std::uint32_t wd = 0;
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) {
+          std::uint32_t c;
+          if constexpr (STREAM == STREAM_U53)
+            c = pert_draw53<GP>(pert53, pick53(x, e), K);
+          else
+            c = pert_draw32<GP>(pert32, pick32(x, e), K);
+          const int q = rem - 1 - static_cast<int>(e);
+          c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+          wd |= c << (e * K);
+        }
+        if (rem <= static_cast<int>(DPB) && h.has_leaf) {  // the leaf draw is element rem
+          const std::uint32_t el = static_cast<std::uint32_t>(rem);
+          if (el < DPB) {
+            if constexpr (STREAM == STREAM_U53)
+              leaf = pick53(x, el).raw() > h.leaf_thr53;
+            else
+              leaf = !h.leaf_never && pick32(x, el) > h.leaf_thr32;
+          }
+        }
+        if (__builtin_expect(wd != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58), word b alone
+          flip = true;
+          Sc[b] ^= wd;
+        }
+      }
+    };
     if (h.pert_mode != 0)  // plan-uniform
       phase_a(std::true_type{});
+    else if (STREAM == STREAM_U53 && rp.phase_a_words && h.k * DPB == 32)
+      phase_a_words();
     else
       phase_a(std::false_type{});
     const bool any_flip = __ballot_sync(smask, flip) != 0;
@@ -604,7 +617,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 2 * LPT) {
           jbase = j0;
           const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
-          *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
+          if constexpr (HI)
+            *reinterpret_cast<uint2*>(dbuf + 2 * r) = make_uint2(x.y, x.w);
+          else
+            *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
           __syncwarp(smask);
           single_pair(Sc, Sn, wreg, j0, 0);
           __syncwarp(smask);
@@ -632,7 +648,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
           // (blocks past the region's last draw are stored too: never read)
-          *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
+          if constexpr (HI)  // high words only (the fast paths read r53 >> 21)
+            *reinterpret_cast<uint2*>(dbuf + 2 * (q * LPT + r)) = make_uint2(xb[q].y, xb[q].w);
+          else
+            *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
         __syncwarp(smask);
         if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
 #pragma unroll

@@ -43,6 +43,22 @@ def run_sharded(simulate, n_total: int, world: int, rank: int, device=None):
     return allreduce_totals(local, device)
 
 
+def run_sharded_nodes(simulate, n_total: int, n_kept: int, world: int, rank: int, device=None):
+    """simulate(traj_begin, n_traj) -> (counts (n_traj, 8), one-counts (n_traj, n_kept)).
+    The job-wide pooled totals (8,) and pooled per-node one-counts (n_kept,),
+    combined in ONE all-reduce of the concatenated vector (the C-ABI device
+    group, csrc/group.cpp, does the same with one ncclAllReduce)."""
+    begin, count = shard_range(n_total, world, rank)
+    vec = np.zeros(COUNT_FIELDS + n_kept, np.int64)
+    if count:
+        cnt, nc = simulate(begin, count)
+        vec[:COUNT_FIELDS] = pooled(cnt)
+        vec[COUNT_FIELDS:] = np.asarray(nc, np.uint64).reshape(-1, n_kept).sum(
+            axis=0, dtype=np.uint64).astype(np.int64)
+    out = allreduce_totals(vec, device)
+    return out[:COUNT_FIELDS], out[COUNT_FIELDS:]
+
+
 # ----------------------------------------------------------------------------
 # Pooled steady-state estimate across ranks (SURVEY §8e: "the estimator does
 # one all-reduce per round"). The C++ estimator (pbn_estimate_with_backend)

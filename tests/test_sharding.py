@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_1605_00854_b200.ensemble import pooled, run_sharded, shard_range
+from paper_1605_00854_b200.ensemble import pooled, run_sharded, run_sharded_nodes, shard_range
 
 
 def test_shard_ranges_partition_ids():
@@ -127,3 +127,51 @@ def test_two_rank_estimate_equals_single_process():
         pb.make_request(precision=0.02, pilot=300, seed=3, n_traj=40))
     for k in ("estimate", "sample_size_used", "burn_in_used", "kappa", "steps_per_traj"):
         assert res[0][k] == res[1][k] == single[k], k
+
+
+def _nodes_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+
+    import oracle
+    import paper_1605_00854_b200 as pb
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, terms = pb.generate_model(96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607)
+    plan = pb.prepare(model, 1 << 25, 16, 8)
+    pred = plan.compile_predicate(terms)
+    orc = oracle.Oracle()
+
+    def sim(b, c):
+        _, cnt, nc = orc.simulate(plan.view, 42, b, c, 250, pred=pred, node_counts=True)
+        return cnt, nc
+
+    tot, nodes = run_sharded_nodes(sim, 29, plan.n_kept, world, rank)
+    out_q.put((rank, (tot.tolist(), nodes.tolist())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_node_counts_equal_single_process():
+    """Per-node one-counts (engine.hpp:378-379) pooled over ranks with the
+    same single all-reduce as the counts (concatenated vector)."""
+    import oracle
+    import paper_1605_00854_b200 as pb
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nodes_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    model, terms = pb.generate_model(96, (1, 2), (2, 5), 0.001, 0.3, 2, False, 1607)
+    plan = pb.prepare(model, 1 << 25, 16, 8)
+    pred = plan.compile_predicate(terms)
+    _, cnt, nc = oracle.Oracle().simulate(plan.view, 42, 0, 29, 250, pred=pred, node_counts=True)
+    want = (pooled(cnt).tolist(), nc.sum(axis=0, dtype=np.uint64).astype(np.int64).tolist())
+    assert res[0] == want and res[1] == want
+    assert sum(want[1]) > 0
