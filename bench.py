@@ -581,7 +581,7 @@ def run_ours(a):
     # Ceiling the injected stream imposes: a kernel doing
     # nothing but generating the workload's Philox4x32-10 blocks, at the
     # measured Philox-only rate of a B200.
-    dpb = 2 if stream == pb.STREAM_U53 else 4
+    dpb = 4  # both streams: 4 high words per Philox block (U53 low words only on ties)
     n_alias = int(np.count_nonzero(flat.grp_alias_size))
     has_leaf = 1 if a.method != "old" else 0
     blocks = (-(-(flat.pert_groups + has_leaf) // dpb)) * traj_steps + (-(-n_alias // dpb)) * fn_total

@@ -53,7 +53,8 @@ extern "C" {
 #define PBN_ECUDA 4
 
 /* Random stream kinds (how a Philox block is cut into next_double() values). */
-#define PBN_STREAM_U53 0 /* 2 draws per Philox block: ((x[2e+1]<<32|x[2e]) >> 11) * 2^-53, as rng.hpp:35 */
+#define PBN_STREAM_U53 0 /* 4 draws per block position b: ((H[e]<<32|L[e]) >> 11) * 2^-53 (rng.hpp:35),
+                            H = Philox block b, L = Philox block b | 2^31          */
 #define PBN_STREAM_U32 1 /* 4 draws per Philox block: x[e] * 2^-32 (fast stream)                      */
 
 /* Per-trajectory statistics record, PBN_COUNT_FIELDS uint64 each. */

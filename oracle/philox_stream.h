@@ -13,9 +13,11 @@
  * Stream layout:
  *   key     = (seed lo32, seed hi32)
  *   counter = (trajectory tau, draw block b, step lo32, step hi32)
- *   U53: 2 draws per block, draw e in {0,1}: ((x[2e+1] << 32 | x[2e]) >> 11) * 2^-53
- *        — the same 53-bit conversion as xoshiro256::next_double (rng.hpp:35)
- *   U32: 4 draws per block, draw e in {0..3}: x[e] * 2^-32
+ *   4 draws per block position b, draw e in {0..3}:
+ *   U53: ((H[e] << 32 | L[e]) >> 11) * 2^-53 with H = block b, L = block
+ *        b | 0x80000000 ("low block") — the same 53-bit conversion as
+ *        xoshiro256::next_double (rng.hpp:35) of the 64-bit word H:L
+ *   U32: H[e] * 2^-32
  *   Within a step the draws come in two phases (engine.hpp:255-312):
  *     phase A = the perturbation draws and the leaf draw (g + 1 draws for the
  *               grouped stepper; n for Method_old, n' + 1 for Method_reduction):
@@ -63,14 +65,16 @@ typedef struct orc_stream {
   uint64_t nb0;      /* first phase-B block: ceil(g1 / DPB) */
   uint64_t cached_block;
   int have_block;
-  uint32_t x[4];
+  uint32_t x[4];  /* high block */
+  uint32_t y[4];  /* low block (U53) */
 } orc_stream;
 
 /* g1 = number of phase-A draws per step: g + 1 for the grouped stepper (g
  * pattern draws + leaf draw), n for Method_old, n' + 1 for Method_reduction. */
 static inline void orc_stream_init(orc_stream* s, uint64_t seed, uint32_t traj, int kind,
                                    uint32_t g1) {
-  const uint64_t dpb = kind == 0 ? 2 : 4;
+  const uint64_t dpb = 4;
+  (void)kind;
   s->g1 = g1;
   s->nb0 = (s->g1 + dpb - 1) / dpb;
   s->seed = seed;
@@ -90,17 +94,22 @@ static inline void orc_stream_begin_step(orc_stream* s, uint64_t step) {
 
 /* Raw draw d of the current step as an integer: r53 (U53) or r32 (U32). */
 static inline uint64_t orc_stream_raw(orc_stream* s, uint64_t d) {
-  const uint64_t dpb = s->kind == 0 ? 2 : 4;
+  const uint64_t dpb = 4;
   const uint64_t b = d < s->g1 ? d / dpb : s->nb0 + (d - s->g1) / dpb;
   const unsigned e = (unsigned)(d < s->g1 ? d % dpb : (d - s->g1) % dpb);
   if (!s->have_block || s->cached_block != b) {
-    const uint32_t ctr[4] = {s->traj, (uint32_t)b, (uint32_t)s->step, (uint32_t)(s->step >> 32)};
     const uint32_t key[2] = {(uint32_t)s->seed, (uint32_t)(s->seed >> 32)};
+    const uint32_t ctr[4] = {s->traj, (uint32_t)b, (uint32_t)s->step, (uint32_t)(s->step >> 32)};
     orc_philox4x32_10(ctr, key, s->x);
+    if (s->kind == 0) {
+      const uint32_t ctr_lo[4] = {s->traj, (uint32_t)b | 0x80000000u, (uint32_t)s->step,
+                                  (uint32_t)(s->step >> 32)};
+      orc_philox4x32_10(ctr_lo, key, s->y);
+    }
     s->cached_block = b;
     s->have_block = 1;
   }
-  if (s->kind == 0) return (((uint64_t)s->x[2 * e + 1] << 32) | s->x[2 * e]) >> 11;
+  if (s->kind == 0) return (((uint64_t)s->x[e] << 32) | s->y[e]) >> 11;
   return s->x[e];
 }
 

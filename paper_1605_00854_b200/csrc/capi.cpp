@@ -125,11 +125,6 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // Lane kernel: scan phase A ahead per lane when fewer steps than this reach
 // the function phase (c1: 0.37 -> +22%; c3: 0.91 -> -17%).
 constexpr double kScanBelow = 0.65;
-// Word-per-block phase A above this per-group flip probability.
-#ifndef PBN_WORDS_ABOVE
-#define PBN_WORDS_ABOVE 0.01
-#endif
-constexpr double kWordsAbove = PBN_WORDS_ABOVE;
 
 // Probability that a step reaches the function phase: no kept node flips
 // (every pattern draw returns 0, or every Bernoulli draw misses) and the leaf
@@ -328,13 +323,7 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
   rp.node_counts = nc ? d_node_counts : nullptr;
   ck(cudaSetDevice(g.device), "cudaSetDevice");
   const launch_choice c = choose_launch(g, a.n_traj, nc);
-  // word-per-block phase A (U53): pays when groups flip often or a lane owns
-  // several phase-A blocks (c5: +2..11 % over p = 1e-4..0.1; c2, one block per
-  // lane and 1.6 % of groups flipping: +0.2 %)
-  {
-    const std::uint32_t blocks53 = (g.ep.h.g + g.ep.h.has_leaf + 1) / 2;
-    rp.phase_a_words = (g.p_group_flip > kWordsAbove || blocks53 > c.lpt) ? 1u : 0u;
-  }
+
   g.last_lpt = c.lpt;
   g.last_warps = c.warps;
   g.last_place = c.place;

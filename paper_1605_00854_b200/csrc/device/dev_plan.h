@@ -156,7 +156,7 @@ struct dev_run_params {
   std::uint64_t series_stride;  // u32 words per trajectory row
   std::uint64_t series_bit0;
   std::uint32_t series_init;
-  std::uint32_t phase_a_words;  // 1: word-per-block phase A (k * DPB == 32, frequent flips)
+  std::uint32_t reserved0;
   // optional per-node one-counts (engine.hpp:378-379): n_traj x n_kept u64,
   // accumulated (+=) over the call's steps
   std::uint64_t* node_counts;

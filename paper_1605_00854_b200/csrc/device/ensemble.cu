@@ -52,8 +52,8 @@ constexpr int kMaxWarpsLpt32 = 28;
 // (general groups gather from shared memory: they run under divergence).
 template <int LPT, int STREAM, int PLACE, int GM>
 __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
-    pbn_ensemble_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
-                        const dev_run_params rp, std::uint64_t* __restrict__ states,
+    pbn_ensemble_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
+                        const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
                         std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
@@ -64,9 +64,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool RG = GM >= 1;
   constexpr bool RG2 = GM == 3;
   constexpr bool SC = GM == 2;
-  // U53 compact kernels keep only the draws' high words in the chunk buffer
-  // (c2 +2.4 %; the general-path kernels lose 2-5 % to the recompute path)
-  constexpr bool HI = STREAM == STREAM_U53 && SC;
 
   const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
@@ -167,21 +164,23 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     return rp.pred.n != 0 && __all_sync(smask, ok) ? 1u : 0u;
   };
 
-  // the step's Philox constants and the first draw of the current phase-B
-  // chunk (the exact path recomputes a draw's low word from them)
+  // the step's Philox constants (the redo path recomputes draws from them)
   step_philox sp{};
-  std::uint32_t jbase = 0;
+  // U53: a combined-function choice made on the draw's high word alone is
+  // exact unless the draw sits on a cell boundary or ties the cut point
+  // (about N+1 draws in 2^32, dev_plan.h acell) or the group/launch takes the
+  // FP64 path. The hot loops only OR such events into `rare_acc`; a function
+  // phase in which any lane saw one is recomputed exactly (redo_fn_phase).
+  bool rare_acc = false;
 
   // Combined-function choice of alias group (engine.hpp:284-291) from draw jj
-  // of the draw buffer, fast form: U53 integer cells (dev_plan.h a53) — `rare`
-  // is set for draws on a cell boundary (about N in 2^32) and for launches or
-  // groups that take the FP64 path, whose choice alias_exact then recomputes;
-  // U32 integer cells (exact, never rare). Branch-free, so the two groups of a
-  // round pair keep independent dependency chains.
+  // of the draw buffer (the draws' high words), fast form: U53 integer cells
+  // (dev_plan.h a53), U32 integer cells (exact, never rare). Branch-free, so
+  // the two groups of a round pair keep independent dependency chains.
   auto alias_fast = [&](const uint4* cells, std::uint32_t asz, std::uint32_t ab,
                         std::uint32_t jj, bool& rare) -> std::uint32_t {
     if constexpr (STREAM == STREAM_U53) {
-      const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];  // x[2e+1]: bits [21, 53) of r53
+      const std::uint32_t hi = dbuf[jj];  // the draw's high word: bits [21, 53) of r53
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * asz;
       const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
       const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(cells + ab + e));  // {alias, hi32(C)}
@@ -195,27 +194,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       return static_cast<std::uint32_t>(P) < cell.x ? c : cell.y;
     }
   };
-  // u*N, truncation, clamp, fraction vs cut-off in IEEE double without
-  // contraction, exactly as engine.hpp:285-290 computes it (U53 only).
-  auto alias_exact = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj) -> std::uint32_t {
-    raw53 rw{dbuf[2 * jj + 1], dbuf[2 * jj]};
-    if constexpr (HI) {  // the chunk keeps only the draws' high words: recompute the block
-      const std::uint32_t d = jbase + jj;  // draw index within the alias region
-      rw = pick53(philox_block(sp, nb0 + d / DPB, rp.rk0, rp.rk1), d % DPB);
-    }
-    const double u = __ull2double_rn(rw.value()) * 0x1.0p-53;
-    const double xx = __dmul_rn(u, __uint2double_rn(asz));
-    std::uint32_t c = __double2uint_rz(xx);
-    if (c >= asz) c = asz - 1;
-    const double fr = __dsub_rn(xx, __uint2double_rn(c));
-    return fr < __ldg(acut + ab + c) ? c : __ldg(aidx + ab + c);
-  };
   auto alias_pick = [&](std::uint32_t asz, std::uint32_t ab, std::uint32_t jj,
                         bool exact) -> std::uint32_t {
     bool rare = exact;
-    std::uint32_t c = alias_fast(acell, asz, ab, jj, rare);  // ab relative to cell_base
-    if constexpr (STREAM == STREAM_U53)
-      if (__builtin_expect(rare, 0)) c = alias_exact(asz, ab + h.cell_base, jj);
+    const std::uint32_t c = alias_fast(acell, asz, ab, jj, rare);  // ab relative to cell_base
+    if constexpr (STREAM == STREAM_U53) rare_acc = rare_acc || rare;
     return c;
   };
 
@@ -255,22 +238,10 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     }
     return v;
   };
-  auto eval_group = [&](const std::uint32_t* Sc, std::uint32_t gi, std::uint32_t jj,
-                        std::uint32_t& olo, std::uint32_t& ohi, std::uint32_t& off,
-                        std::uint32_t& members, auto uni_c) {
-    constexpr bool UNI = decltype(uni_c)::value && RG && !RG2 && LPT == 32;
-    const uint4 G = ldp<GC>(groups + gi);
-    const std::uint32_t asz = G.w & 0x7FFFFFu;
-    members = (G.w >> 24) + 1;
-    off = G.x;
-    const std::uint32_t idx =
-        asz != 0 ? alias_pick(asz, G.z, jj, exact_all || (G.w & kGroupExactAlias)) : 0u;
-    const uint4 F = ldp<GC>(fns + G.y + idx);
-    std::uint32_t v;
-    if constexpr (UNI)
-      v = gather_fn_shfl(F);
-    else
-      v = gather_fn(Sc, F);
+  // Packed member outputs of combined function F at parent valuation v
+  // (engine.hpp:303): inline table or an entry of 1/2/4/8 bytes.
+  auto table_out = [&](const uint4& F, std::uint32_t v, std::uint32_t members, std::uint32_t& olo,
+                       std::uint32_t& ohi) {
     ohi = 0;
     if (F.y & 0x80u) {  // inline table
       const std::uint32_t m = members >= 32 ? 0xFFFFFFFFu : ((1u << members) - 1u);
@@ -290,6 +261,35 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       ohi = o.y;
     }
   };
+  // OR a group's packed outputs into the next state at bit `off` with shared
+  // atomics (engine.hpp:304-309; up to 64 members span three words)
+  auto emit_atomic = [&](std::uint32_t* Sn, std::uint32_t olo, std::uint32_t ohi, std::uint32_t off) {
+    const std::uint32_t w = off >> 5, sh = off & 31;
+    const std::uint32_t a0 = olo << sh;
+    const std::uint32_t a1 = sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
+    const std::uint32_t a2 = sh ? (ohi >> (32 - sh)) : 0u;
+    if (a0) atomicOr(Sn + w, a0);
+    if (a1) atomicOr(Sn + w + 1, a1);
+    if (a2) atomicOr(Sn + w + 2, a2);
+  };
+  auto eval_group = [&](const std::uint32_t* Sc, std::uint32_t gi, std::uint32_t jj,
+                        std::uint32_t& olo, std::uint32_t& ohi, std::uint32_t& off,
+                        std::uint32_t& members, auto uni_c) {
+    constexpr bool UNI = decltype(uni_c)::value && RG && !RG2 && LPT == 32;
+    const uint4 G = ldp<GC>(groups + gi);
+    const std::uint32_t asz = G.w & 0x7FFFFFu;
+    members = (G.w >> 24) + 1;
+    off = G.x;
+    const std::uint32_t idx =
+        asz != 0 ? alias_pick(asz, G.z, jj, exact_all || (G.w & kGroupExactAlias)) : 0u;
+    const uint4 F = ldp<GC>(fns + G.y + idx);
+    std::uint32_t v;
+    if constexpr (UNI)
+      v = gather_fn_shfl(F);
+    else
+      v = gather_fn(Sc, F);
+    table_out(F, v, members, olo, ohi);
+  };
 
   // OR one round's outputs into the next state (engine.hpp:304-309). A round
   // of single-node groups covers consecutive bits: one ballot builds the word.
@@ -308,13 +308,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         if (sh && (bits >> (32 - sh))) atomicOr(Sn + w + 1, bits >> (32 - sh));
       }
     } else if (act) {
-      const std::uint32_t w = off >> 5, sh = off & 31;
-      const std::uint32_t a0 = olo << sh;
-      const std::uint32_t a1 = sh ? (olo >> (32 - sh)) | (ohi << sh) : ohi;
-      const std::uint32_t a2 = sh ? (ohi >> (32 - sh)) : 0u;
-      if (a0) atomicOr(Sn + w, a0);
-      if (a1) atomicOr(Sn + w + 1, a1);
-      if (a2) atomicOr(Sn + w + 2, a2);
+      emit_atomic(Sn, olo, ohi, off);
     }
   };
 
@@ -329,12 +323,12 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // records (SC) the byte offset of its scol function record — then its output bit;
   // loads and shuffles only, so two groups can be interleaved by the scheduler.
   auto single_fn = [&](std::uint32_t j, std::uint32_t jj, bool& rare) -> std::uint32_t {
-    rare = exact_all;
+    rare = false;
     if constexpr (SC) {
       const uint4 ar = ldp<GC>(arec4 + j);  // {U53 cell offset, function offset, N, ~N}
       std::uint32_t pick;
       if constexpr (STREAM == STREAM_U53) {
-        const std::uint32_t hi = HI ? dbuf[jj] : dbuf[2 * jj + 1];
+        const std::uint32_t hi = dbuf[jj];
         const std::uint64_t P = static_cast<std::uint64_t>(hi) * ar.z;
         const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
         const uint2 V = ldp<GC>(reinterpret_cast<const uint2*>(core + ar.x + 8 * kScolSlots * e));
@@ -356,15 +350,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       // two groups of a round pair keep independent dependency chains
       return base + alias_fast(acell_s, ar >> 24, base, jj, rare);
     }
-  };
-  auto single_fn_exact = [&](std::uint32_t j, std::uint32_t jj) -> std::uint32_t {
-    const std::uint32_t ar = ldp<GC>(arec + j);
-    const std::uint32_t base = ar & 0xFFFFFFu;
-    const std::uint32_t pick = alias_exact(ar >> 24, base, jj);
-    if constexpr (SC)
-      return ldp<GC>(arec4 + j).y + 8 * kScolSlots * pick;
-    else
-      return base + pick;
   };
   auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
     if constexpr (SC) {
@@ -405,9 +390,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   auto single_bit = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t j,
                         std::uint32_t jj) -> bool {
     bool rare;
-    std::uint32_t f = single_fn(j, jj, rare);
-    if constexpr (STREAM == STREAM_U53)
-      if (__builtin_expect(rare, 0)) f = single_fn_exact(j, jj);
+    const std::uint32_t f = single_fn(j, jj, rare);
+    if constexpr (STREAM == STREAM_U53) rare_acc = rare_acc || rare;
     return single_out(Sc, wreg, f);
   };
   // A single-node round's ballot word lands at bit jr of the next state.
@@ -431,14 +415,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                          std::uint32_t jr0, std::uint32_t t) {
     const std::uint32_t jr1 = jr0 + LPT;
     bool rare0, rare1;
-    std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
-    std::uint32_t f1 = single_fn(jr1 + r, (t + 1) * LPT + r, rare1);
-    if constexpr (STREAM == STREAM_U53) {
-      if (__builtin_expect(rare0 || rare1, 0)) {
-        if (rare0) f0 = single_fn_exact(jr0 + r, t * LPT + r);
-        if (rare1) f1 = single_fn_exact(jr1 + r, (t + 1) * LPT + r);
-      }
-    }
+    const std::uint32_t f0 = single_fn(jr0 + r, t * LPT + r, rare0);
+    const std::uint32_t f1 = single_fn(jr1 + r, (t + 1) * LPT + r, rare1);
+    if constexpr (STREAM == STREAM_U53) rare_acc = rare_acc || rare0 || rare1;
     const bool b0 = single_out(Sc, wreg, f0);
     const bool b1 = single_out(Sc, wreg, f1);
     store_bits(Sn, jr0, __ballot_sync(smask, b0), true);
@@ -453,19 +432,77 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     std::uint32_t f[4];
 #pragma unroll
     for (std::uint32_t u = 0; u < 4; ++u) f[u] = single_fn(jr0 + u * LPT + r, (t + u) * LPT + r, rr[u]);
-    if constexpr (STREAM == STREAM_U53) {
-      if (__builtin_expect(rr[0] || rr[1] || rr[2] || rr[3], 0)) {
-#pragma unroll
-        for (std::uint32_t u = 0; u < 4; ++u)
-          if (rr[u]) f[u] = single_fn_exact(jr0 + u * LPT + r, (t + u) * LPT + r);
-      }
-    }
+    if constexpr (STREAM == STREAM_U53) rare_acc = rare_acc || rr[0] || rr[1] || rr[2] || rr[3];
     bool b[4];
 #pragma unroll
     for (std::uint32_t u = 0; u < 4; ++u) b[u] = single_out(Sc, wreg, f[u]);
 #pragma unroll
     for (std::uint32_t u = 0; u < 4; ++u) store_bits(Sn, jr0 + u * LPT, __ballot_sync(smask, b[u]), true);
   };
+
+  // The exact choice of engine.hpp:285-290 in IEEE double without
+  // contraction, from the full 53-bit draw r53 (U53).
+  auto alias_fp64 = [&](std::uint32_t asz, std::uint32_t ab, std::uint64_t r53) -> std::uint32_t {
+    const double u = __ull2double_rn(r53) * 0x1.0p-53;
+    const double xx = __dmul_rn(u, __uint2double_rn(asz));
+    std::uint32_t c = __double2uint_rz(xx);
+    if (c >= asz) c = asz - 1;
+    const double fr = __dsub_rn(xx, __uint2double_rn(c));
+    return fr < __ldg(acut + ab + c) ? c : __ldg(aidx + ab + c);
+  };
+  // Exact recomputation of a function phase (engine.hpp:270-311) whose fast
+  // pass saw a rare U53 choice (rare_acc; ~1e-6 of function phases on c2):
+  // every combined-function draw rebuilt as its full 53 bits (high word from
+  // block b, low word from block b | kLoBlock) and chosen in FP64; parents from
+  // the shared-memory state; outputs ORed into the re-zeroed next state.
+  auto redo_fn_phase = [&](const std::uint32_t* Scur, std::uint32_t* Snext) {
+    for (std::uint32_t w = r; w < sw32; w += LPT) Snext[w] = 0;
+    __syncwarp(smask);
+    for (std::uint32_t gi = r; gi < NG; gi += LPT) {
+      std::uint64_t r53 = 0;
+      if (gi < A) {  // draw gi of phase B (alias groups come first)
+        const std::uint32_t b = nb0 + gi / DPB, e = gi % DPB;
+        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+        const uint4 y = philox_block(sp, b | kLoBlock, rp.rk0, rp.rk1);
+        r53 = ((static_cast<std::uint64_t>(pick32(x, e)) << 32) | pick32(y, e)) >> 11;
+      }
+      uint4 F;
+      std::uint32_t off, members;
+      if (gi < A1) {  // single node at offset gi (dev_plan.h arec; fns_s: absolute indices)
+        const std::uint32_t ar = ldp<GC>(arec + gi);
+        const std::uint32_t base = ar & 0xFFFFFFu;
+        F = fns_s[base + alias_fp64(ar >> 24, base, r53)];
+        off = gi;
+        members = 1;
+      } else {
+        const uint4 G = ldp<GC>(groups + gi);
+        const std::uint32_t asz = G.w & 0x7FFFFFu;
+        members = (G.w >> 24) + 1;
+        off = G.x;
+        F = ldp<GC>(fns + G.y + (asz ? alias_fp64(asz, G.z + h.cell_base, r53) : 0u));
+      }
+      std::uint32_t olo, ohi;
+      table_out(F, gather_fn(Scur, F), members, olo, ohi);
+      emit_atomic(Snext, olo, ohi, off);
+    }
+    __syncwarp(smask);
+  };
+
+  // Phase-A masks of a block's draws (engine.hpp:257-268): full patterns for
+  // groups before the last, the k'-bit mask for the last group (:261),
+  // nothing for the leaf draw and past it; lane r's own first block's masks
+  // are step-invariant and kept in registers.
+  auto pa_mask = [&](std::uint32_t b, std::uint32_t e) -> std::uint32_t {
+    const int q = static_cast<int>(g) - 1 - static_cast<int>(b * DPB + e);
+    return q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+  };
+  auto lf_elem = [&](std::uint32_t b) -> std::uint32_t {  // the leaf draw's element (>= DPB: none)
+    const int e = static_cast<int>(g) - static_cast<int>(b * DPB);
+    return h.has_leaf && e >= 0 && e < static_cast<int>(DPB) ? static_cast<std::uint32_t>(e) : DPB;
+  };
+  static_assert(DPB == 4, "phase A masks are kept as a uint4");
+  const uint4 pam0 = make_uint4(pa_mask(r, 0), pa_mask(r, 1), pa_mask(r, 2), pa_mask(r, 3));
+  const std::uint32_t lfe0 = lf_elem(r);
 
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
@@ -497,91 +534,82 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     // before the last group, the k'-bit mask for the last group (engine.hpp:
     // 261) and nothing for the leaf draw and the block's unused tail.
     bool flip = false, leaf = false;
-    // one Philox block of phase A: draws b*DPB .. b*DPB+DPB-1
-    auto phase_a_block = [&](std::uint32_t b, auto bern_c) {
+    // One Philox block of phase A: draws b*DPB .. b*DPB+DPB-1, each looked up
+    // and masked (pam: full patterns before the last group, the k'-bit mask
+    // for the last group (engine.hpp:261), nothing for the leaf draw and the
+    // block's unused tail); `lfe` is the leaf draw's element (>= DPB: none).
+    // U53: decided on the draws' high words; a tie recomputes the block's
+    // decisions with the low words (one more Philox block, ~2^-14 of blocks
+    // at k = 16). WPB (k * DPB = 32 or 64: k = 8 or 16) — the block's patterns
+    // fill exactly state words b*WPB.., which no other lane touches: they are
+    // XOR-ed in with plain read-modify-writes; otherwise per-draw atomics.
+    auto phase_a_block = [&](std::uint32_t b, const uint4 pam, std::uint32_t lfe,
+                             auto bern_c, auto wpb_c) {
       constexpr bool BERN = decltype(bern_c)::value;  // Method_old / Method_reduction plans
+      constexpr std::uint32_t WPB = decltype(wpb_c)::value;
       const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-      const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
+      std::uint32_t c[DPB];
+      bool rare = false, lf = false;
 #pragma unroll
-      for (std::uint32_t e = 0; e < DPB; ++e) {
-        std::uint32_t c;
-        if constexpr (BERN) {  // per-node flip iff u < p (engine.hpp:198)
-          if constexpr (STREAM == STREAM_U53)
-            c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
-          else
-            c = pick32(x, e) < h.pthr32 ? 1u : 0u;
-        } else if constexpr (STREAM == STREAM_U53) {
-          c = pert_draw53<GP>(pert53, pick53(x, e), k);
-        } else {
-          c = pert_draw32<GP>(pert32, pick32(x, e), k);
+      for (std::uint32_t e = 0; e < DPB; ++e)
+        c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), false, 0u, rare);
+      if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
+      if constexpr (STREAM == STREAM_U53) {
+        if (__builtin_expect(rare, 0)) {
+          const uint4 y = philox_lo_block(sp, b, rp.rk0, rp.rk1);
+          bool unused = false;
+#pragma unroll
+          for (std::uint32_t e = 0; e < DPB; ++e)
+            c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), true, pick32(y, e), unused);
+          if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), true, pick32(y, lfe), unused);
         }
-        const int q = rem - 1 - static_cast<int>(e);
-        c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
-        if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+      }
+      leaf = leaf || lf;
+      if constexpr (WPB == 2) {  // k = 16: elements 0,1 -> word 2b, elements 2,3 -> word 2b+1
+        const std::uint32_t w0 = (c[0] & pam.x) | ((c[1] & pam.y) << 16);
+        const std::uint32_t w1 = (c[2] & pam.z) | ((c[3] & pam.w) << 16);
+        if (__builtin_expect((w0 | w1) != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
           flip = true;
-          const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
-          atomicXor(Sc + w, c << sh);
-          if (sh != 0 && (c >> (32 - sh)) != 0) atomicXor(Sc + w + 1, c >> (32 - sh));
+          Sc[2 * b] ^= w0;
+          Sc[2 * b + 1] ^= w1;
         }
-        if (q == -1 && h.has_leaf) {  // this element is the leaf draw (engine.hpp:268)
-          if constexpr (STREAM == STREAM_U53)
-            leaf = pick53(x, e).raw() > h.leaf_thr53;
-          else
-            leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
+      } else if constexpr (WPB == 1) {  // k = 8: the block's four patterns are word b
+        const std::uint32_t w0 = (c[0] & pam.x) | ((c[1] & pam.y) << 8) |
+                                 ((c[2] & pam.z) << 16) | ((c[3] & pam.w) << 24);
+        if (__builtin_expect(w0 != 0, 0)) {
+          flip = true;
+          Sc[b] ^= w0;
         }
-      }
-    };
-    auto phase_a = [&](auto bern_c) {
-      if (nb0 <= LPT) {  // launch-uniform: at most one block per lane
-        if (r < nb0) phase_a_block(r, bern_c);
       } else {
-        for (std::uint32_t b = r; b < nb0; b += LPT) phase_a_block(b, bern_c);
-      }
-    };
-    // k * DPB == 32 (U53 with k = 16, U32 with k = 8): block b's patterns
-    // fill exactly state word b, which no other lane touches — the patterns
-    // are OR-ed into one word and XOR-ed in with a plain read-modify-write
-    // instead of per-draw atomics (c5 at p = 0.1 flips ~3 groups per lane and
-    // step). Masks only matter in the block of the last group / leaf draw.
-    auto phase_a_words = [&]() {
-      if constexpr (STREAM != STREAM_U53) return;  // U53 only (U32 kernels keep their code)
-      constexpr std::uint32_t K = 32 / DPB;
-      for (std::uint32_t b = r; b < nb0; b += LPT) {
-        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-        const int rem = static_cast<int>(g) - static_cast<int>(b * DPB);  // pert draws left
-        std::uint32_t wd = 0;
 #pragma unroll
         for (std::uint32_t e = 0; e < DPB; ++e) {
-          std::uint32_t c;
-          if constexpr (STREAM == STREAM_U53)
-            c = pert_draw53<GP>(pert53, pick53(x, e), K);
-          else
-            c = pert_draw32<GP>(pert32, pick32(x, e), K);
-          const int q = rem - 1 - static_cast<int>(e);
-          c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
-          wd |= c << (e * K);
-        }
-        if (rem <= static_cast<int>(DPB) && h.has_leaf) {  // the leaf draw is element rem
-          const std::uint32_t el = static_cast<std::uint32_t>(rem);
-          if (el < DPB) {
-            if constexpr (STREAM == STREAM_U53)
-              leaf = pick53(x, el).raw() > h.leaf_thr53;
-            else
-              leaf = !h.leaf_never && pick32(x, el) > h.leaf_thr32;
+          const std::uint32_t ce = c[e] & pick32(pam, e);
+          if (__builtin_expect(ce != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+            flip = true;
+            const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
+            atomicXor(Sc + w, ce << sh);
+            if (sh != 0 && (ce >> (32 - sh)) != 0) atomicXor(Sc + w + 1, ce >> (32 - sh));
           }
         }
-        if (__builtin_expect(wd != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58), word b alone
-          flip = true;
-          Sc[b] ^= wd;
-        }
+      }
+    };
+    auto phase_a = [&](auto bern_c, auto wpb_c) {
+      if (nb0 <= LPT) {  // launch-uniform: at most one block per lane (masks precomputed)
+        if (r < nb0) phase_a_block(r, pam0, lfe0, bern_c, wpb_c);
+      } else {
+        for (std::uint32_t b = r; b < nb0; b += LPT)
+          phase_a_block(b, make_uint4(pa_mask(b, 0), pa_mask(b, 1), pa_mask(b, 2), pa_mask(b, 3)),
+                        lf_elem(b), bern_c, wpb_c);
       }
     };
     if (h.pert_mode != 0)  // plan-uniform
-      phase_a(std::true_type{});
-    else if (STREAM == STREAM_U53 && rp.phase_a_words && h.k * DPB == 32)
-      phase_a_words();
+      phase_a(std::true_type{}, std::integral_constant<std::uint32_t, 0>{});
+    else if (k == 16)
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 2>{});
+    else if (k == 8)
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 1>{});
     else
-      phase_a(std::false_type{});
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 0>{});
     const bool any_flip = __ballot_sync(smask, flip) != 0;
     const bool any_leaf = __ballot_sync(smask, leaf) != 0;
 
@@ -596,6 +624,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       // votes do not order shared memory; a plan without alias groups goes
       // straight to the plain region's atomics)
       __syncwarp(smask);
+      rare_acc = exact_all;
       std::uint32_t wreg = 0;  // RG: state word `lane` of the current state
       if constexpr (RG) wreg = lane < sw32 ? Sc[lane] : 0u;
       wreg_s = wreg;
@@ -615,12 +644,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         // bookkeeping; the general loop below takes the remaining chunks
         const std::uint32_t jfull = A1 & ~(2u * LPT - 1u);
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 2 * LPT) {
-          jbase = j0;
           const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
-          if constexpr (HI)
-            *reinterpret_cast<uint2*>(dbuf + 2 * r) = make_uint2(x.y, x.w);
-          else
-            *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
+          *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
           __syncwarp(smask);
           single_pair(Sc, Sn, wreg, j0, 0);
           __syncwarp(smask);
@@ -630,7 +655,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         // U32 compact: chunks of one single-node quad
         const std::uint32_t jfull = A1 & ~(4u * LPT - 1u);
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 4 * LPT) {
-          jbase = j0;
           *reinterpret_cast<uint4*>(dbuf + 4 * r) = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
           __syncwarp(smask);
           single_quad(Sc, Sn, wreg, j0, 0);
@@ -639,7 +663,6 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         jstart = jfull;
       }
       for (std::uint32_t j0 = jstart; j0 < A; j0 += LPT * DPB * CB) {
-        jbase = j0;
         if constexpr (!kPhiloxPipeline) {
 #pragma unroll
           for (std::uint32_t q = 0; q < CB; ++q)
@@ -648,10 +671,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
           // (blocks past the region's last draw are stored too: never read)
-          if constexpr (HI)  // high words only (the fast paths read r53 >> 21)
-            *reinterpret_cast<uint2*>(dbuf + 2 * (q * LPT + r)) = make_uint2(xb[q].y, xb[q].w);
-          else
-            *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
+          *reinterpret_cast<uint4*>(dbuf + 4 * (q * LPT + r)) = xb[q];
         __syncwarp(smask);
         if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
 #pragma unroll
@@ -736,6 +756,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         if (gr + LPT < NG) emit_round(Sn, a1, lo1, hi1, off1, m1);
       }
       __syncwarp(smask);
+      if constexpr (STREAM == STREAM_U53)
+        if (__builtin_expect(__any_sync(smask, rare_acc), 0)) redo_fn_phase(Sc, Sn);
       cur ^= 1;
       ++nfn;
     }

@@ -132,12 +132,36 @@ __device__ __forceinline__ std::uint32_t state_word_mask(std::uint32_t n, std::u
   return lo + 32 <= n ? 0xFFFFFFFFu : lo >= n ? 0u : (1u << (n - lo)) - 1u;
 }
 
+// Both streams take 4 draws per Philox block: word e of block b is the high
+// word of draw 4b + e (U32: the whole draw; U53: its low word is word e of
+// block b | kLoBlock, philox.cuh).
 template <int STREAM>
 struct draws {
-  static constexpr std::uint32_t kPerBlock = STREAM == STREAM_U53 ? 2 : 4;
+  static constexpr std::uint32_t kPerBlock = 4;
 };
 
-// Raw draw e of a Philox block: r53 as (hi32, lo21) pieces for U53, r32 for U32.
+// The low block of block position b (U53 rare paths). Out of line: the hot
+// paths keep the registers a second inlined Philox block would take.
+static __device__ __noinline__ uint4 philox_lo_block(step_philox sp, std::uint32_t b,
+                                              const std::uint32_t* rk0, const std::uint32_t* rk1) {
+  return philox_block(sp, b | kLoBlock, rk0, rk1);
+}
+
+// Low word of draw e of block b (U53; U32 draws have none): the rare paths.
+template <int STREAM>
+__device__ __forceinline__ std::uint32_t lo_word(const step_philox& sp, std::uint32_t b,
+                                                 std::uint32_t e, const std::uint32_t* rk0,
+                                                 const std::uint32_t* rk1) {
+  if constexpr (STREAM == STREAM_U53) {
+    const uint4 y = philox_lo_block(sp, b, rk0, rk1);
+    return e == 0 ? y.x : e == 1 ? y.y : e == 2 ? y.z : y.w;
+  } else {
+    return 0u;
+  }
+}
+
+// Raw draw: r53 as (hi32, lo21) pieces (U32: lo = 0, r53 = r32 << 21, the
+// same double r32 * 2^-32).
 struct raw53 {
   std::uint32_t hi;  // bits [21, 53) of r53  (= x[2e+1])
   std::uint32_t lo;  // x[2e]; bits [0, 21) of r53 are lo >> 11
@@ -150,26 +174,59 @@ struct raw53 {
   }
 };
 
-__device__ __forceinline__ raw53 pick53(const uint4& x, std::uint32_t e) {
-  return e == 0 ? raw53{x.y, x.x} : raw53{x.w, x.z};
-}
 __device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e) {
   return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
 }
 
 // Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form on
-// the raw draw word: the cell index is the top k bits, the threshold compare
-// runs on the remaining 64-k bits (dev_plan.h pert53).
+// the raw draw word R = hi << 32 | lo: the cell index is the top k bits, the
+// threshold compare runs on the remaining 64-k bits (dev_plan.h pert53).
+// Fast form on the high word alone: decided unless its 32-k compare bits tie
+// with the cell's (`rare`; pert_draw53_exact then needs the low word).
 template <bool G>
-__device__ __forceinline__ std::uint32_t pert_draw53(const std::uint64_t* cells, raw53 r,
-                                                     std::uint32_t k) {
+__device__ __forceinline__ std::uint32_t pert_draw53_hi(const std::uint64_t* cells, std::uint32_t hi,
+                                                        std::uint32_t k, bool& rare) {
+  const std::uint32_t c = hi >> (32 - k);
+  const std::uint32_t hmask = 0xFFFFFFFFu >> k;
+  const std::uint32_t ehi = ldp<G>(reinterpret_cast<const std::uint32_t*>(cells + c) + 1);
+  const std::uint32_t a = hi & hmask, b = ehi & hmask;
+  rare = rare || a == b;
+  return a < b ? c : (ehi >> (32 - k));
+}
+__device__ __forceinline__ std::uint32_t pert_draw53_exact(const std::uint64_t* cells, raw53 r,
+                                                           std::uint32_t k) {
   const std::uint32_t c = r.hi >> (32 - k);
   const std::uint32_t hmask = 0xFFFFFFFFu >> k;
-  const std::uint64_t e = ldp<G>(cells + c);
+  const std::uint64_t e = cells[c];  // generic load: smem or global
   const std::uint32_t ehi = static_cast<std::uint32_t>(e >> 32);
   const std::uint64_t rl = (static_cast<std::uint64_t>(r.hi & hmask) << 32) | r.lo;
   const std::uint64_t el = (static_cast<std::uint64_t>(ehi & hmask) << 32) | static_cast<std::uint32_t>(e);
   return rl < el ? c : (ehi >> (32 - k));
+}
+
+// One phase-A draw (engine.hpp:257-266) from its high word hw: the
+// perturbation pattern, or (BERN, node-wise plans) 1 iff u < p (engine.hpp:198).
+// U53 fast form (exact = false) sets `rare` when the high word ties with the
+// threshold; the exact form then decides with the low word lo. U32: lo = 0,
+// never rare.
+template <int STREAM, bool G, bool BERN>
+__device__ __forceinline__ std::uint32_t pa_draw(const dev_plan_header& h,
+                                                 const std::uint64_t* pert53,
+                                                 const std::uint32_t* pert32, std::uint32_t k,
+                                                 std::uint32_t hw, bool exact, std::uint32_t lo,
+                                                 bool& rare);
+// The leaf draw (engine.hpp:268, reduction.hpp:98): u > t.
+template <int STREAM>
+__device__ __forceinline__ bool pa_leaf(const dev_plan_header& h, std::uint32_t hw, bool exact,
+                                        std::uint32_t lo, bool& rare) {
+  if constexpr (STREAM == STREAM_U53) {
+    if (exact) return ((static_cast<std::uint64_t>(hw) << 32) | lo) > h.leaf_thr53;
+    const std::uint32_t th = static_cast<std::uint32_t>(h.leaf_thr53 >> 32);
+    rare = rare || hw == th;
+    return hw > th;
+  } else {
+    return !h.leaf_never && hw > h.leaf_thr32;
+  }
 }
 
 template <bool G>
@@ -179,6 +236,29 @@ __device__ __forceinline__ std::uint32_t pert_draw32(const std::uint32_t* cells,
   const std::uint32_t lmask = (1u << (32 - k)) - 1;
   const std::uint32_t e = ldp<G>(cells + c);
   return (r & lmask) < (e & lmask) ? c : (e >> (32 - k));
+}
+
+template <int STREAM, bool G, bool BERN>
+__device__ __forceinline__ std::uint32_t pa_draw(const dev_plan_header& h,
+                                                 const std::uint64_t* pert53,
+                                                 const std::uint32_t* pert32, std::uint32_t k,
+                                                 std::uint32_t hw, bool exact, std::uint32_t lo,
+                                                 bool& rare) {
+  if constexpr (BERN) {
+    if constexpr (STREAM == STREAM_U53) {
+      if (exact) return ((static_cast<std::uint64_t>(hw) << 32) | lo) < h.pthr53 ? 1u : 0u;
+      const std::uint32_t ph = static_cast<std::uint32_t>(h.pthr53 >> 32);
+      rare = rare || hw == ph;
+      return hw < ph ? 1u : 0u;
+    } else {
+      return hw < h.pthr32 ? 1u : 0u;
+    }
+  } else if constexpr (STREAM == STREAM_U53) {
+    if (exact) return pert_draw53_exact(pert53, raw53{hw, lo}, k);
+    return pert_draw53_hi<G>(pert53, hw, k, rare);
+  } else {
+    return pert_draw32<G>(pert32, hw, k);
+  }
 }
 
 // Gather 4 parent bits (records r0..r3 packed in two words) into slots b0..b0+3.

@@ -52,8 +52,8 @@ constexpr int kLaneMaxWarps = 28;  // 896 threads: 72 registers per thread
 // ~90% of steps reach it).
 template <int STREAM, int PLACE, bool SCAN>
 __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
-    pbn_lane_kernel(const dev_plan_header h, const std::uint8_t* __restrict__ gblob,
-                    const dev_run_params rp, std::uint64_t* __restrict__ states,
+    pbn_lane_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
+                    const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
                     std::uint64_t* __restrict__ counts) {
   extern __shared__ __align__(16) std::uint8_t smem[];
   __shared__ std::uint64_t stage_bar;
@@ -222,78 +222,92 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     }
   };
 
+  // Phase-A masks (engine.hpp:257-268): full patterns for groups before the
+  // last, the k'-bit mask for the last group (:261), nothing for the leaf
+  // draw and past it; lf_elem: the leaf draw's element of block b (>= DPB: none).
+  auto pa_mask = [&](std::uint32_t b, std::uint32_t e) -> std::uint32_t {
+    const int q = static_cast<int>(g) - 1 - static_cast<int>(b * DPB + e);
+    return q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
+  };
+  auto lf_elem = [&](std::uint32_t b) -> std::uint32_t {
+    const int e = static_cast<int>(g) - static_cast<int>(b * DPB);
+    return h.has_leaf && e >= 0 && e < static_cast<int>(DPB) ? static_cast<std::uint32_t>(e) : DPB;
+  };
+
   // Phase A of step `sp` on state Sc (engine.hpp:257-268): flips XORed in.
   auto phase_a_step = [&](std::uint32_t* Sc, const step_philox& sp, bool& flip, bool& leaf) {
     flip = false;
     leaf = false;
-    // blocks [0, nplain) hold full-width pattern draws only (no per-draw
-    // mask or leaf test); the tail blocks hold the last group and the leaf draw
-    auto phase_a = [&](auto bern_c) {
+    // One Philox block: decisions of its DPB draws on the high words (U53:
+    // a tie recomputes them with the low block), masks, XOR into the lane's
+    // state column. Blocks [0, nplain) hold full-width pattern draws only; the
+    // tail blocks hold the last group (k'-bit mask, engine.hpp:261) and the
+    // leaf draw (warp-uniform masks). WPB (k = 16: 2, k = 8: 1): a block's
+    // patterns fill exactly state words b*WPB.. — XOR each word once.
+    auto block = [&](std::uint32_t b, bool tail, auto bern_c, auto wpb_c) {
       constexpr bool BERN = decltype(bern_c)::value;  // node-wise plans (Method_old / reduction)
-      auto elem = [&](const uint4& x, std::uint32_t b, std::uint32_t e, bool tail) {
-        std::uint32_t c;
-        if constexpr (BERN) {
-          if constexpr (STREAM == STREAM_U53)
-            c = pick53(x, e).raw() < h.pthr53 ? 1u : 0u;
-          else
-            c = pick32(x, e) < h.pthr32 ? 1u : 0u;
-        } else if constexpr (STREAM == STREAM_U53) {
-          c = pert_draw53<GP>(pert53, pick53(x, e), k);
-        } else {
-          c = pert_draw32<GP>(pert32, pick32(x, e), k);
-        }
-        const int q = static_cast<int>(g) - 1 - static_cast<int>(b * DPB + e);
-        if (tail) c &= q > 0 ? 0xFFFFFFFFu : (q == 0 ? h.last_mask : 0u);
-        if (__builtin_expect(c != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
-          flip = true;
-          const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
-          Sc[32 * w] ^= c << sh;
-          if (sh != 0 && (c >> (32 - sh)) != 0) Sc[32 * (w + 1)] ^= c >> (32 - sh);
-        }
-        if (tail && q == -1 && h.has_leaf) {  // the leaf draw (engine.hpp:268)
-          if constexpr (STREAM == STREAM_U53)
-            leaf = pick53(x, e).raw() > h.leaf_thr53;
-          else
-            leaf = !h.leaf_never && pick32(x, e) > h.leaf_thr32;
-        }
-      };
-      if (!BERN && k * DPB == 32) {
-        // k * DPB == 32: a plain block's patterns fill exactly state word b —
-        // OR them and XOR the word once
-        constexpr std::uint32_t K = 32 / DPB;
-        for (std::uint32_t b = 0; b < nplain; ++b) {
-          const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-          std::uint32_t wd = 0;
+      constexpr std::uint32_t WPB = decltype(wpb_c)::value;
+      const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+      const std::uint32_t lfe = tail ? lf_elem(b) : DPB;
+      std::uint32_t c[DPB];
+      bool rare = false, lf = false;
 #pragma unroll
-          for (std::uint32_t e = 0; e < DPB; ++e) {
-            if constexpr (STREAM == STREAM_U53)
-              wd |= pert_draw53<GP>(pert53, pick53(x, e), K) << (e * K);
-            else
-              wd |= pert_draw32<GP>(pert32, pick32(x, e), K) << (e * K);
-          }
-          if (__builtin_expect(wd != 0, 0)) {
-            flip = true;
-            Sc[32 * b] ^= wd;
-          }
+      for (std::uint32_t e = 0; e < DPB; ++e)
+        c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), false, 0u, rare);
+      if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
+      if constexpr (STREAM == STREAM_U53) {
+        if (__builtin_expect(rare, 0)) {
+          const uint4 y = philox_lo_block(sp, b, rp.rk0, rp.rk1);
+          bool unused = false;
+#pragma unroll
+          for (std::uint32_t e = 0; e < DPB; ++e)
+            c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), true, pick32(y, e), unused);
+          if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), true, pick32(y, lfe), unused);
+        }
+      }
+      leaf = leaf || lf;
+      if (tail) {
+#pragma unroll
+        for (std::uint32_t e = 0; e < DPB; ++e) c[e] &= pa_mask(b, e);
+      }
+      if constexpr (WPB == 2) {
+        const std::uint32_t w0 = c[0] | (c[1] << 16), w1 = c[2] | (c[3] << 16);
+        if (__builtin_expect((w0 | w1) != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+          flip = true;
+          Sc[32 * (2 * b)] ^= w0;
+          Sc[32 * (2 * b + 1)] ^= w1;
+        }
+      } else if constexpr (WPB == 1) {
+        const std::uint32_t w0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+        if (__builtin_expect(w0 != 0, 0)) {
+          flip = true;
+          Sc[32 * b] ^= w0;
         }
       } else {
-        for (std::uint32_t b = 0; b < nplain; ++b) {
-          const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
 #pragma unroll
-          for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, false);
+        for (std::uint32_t e = 0; e < DPB; ++e) {
+          const std::uint32_t ce = c[e];
+          if (__builtin_expect(ce != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+            flip = true;
+            const std::uint32_t o = (b * DPB + e) * k, w = o >> 5, sh = o & 31;
+            Sc[32 * w] ^= ce << sh;
+            if (sh != 0 && (ce >> (32 - sh)) != 0) Sc[32 * (w + 1)] ^= ce >> (32 - sh);
+          }
         }
       }
-      for (std::uint32_t b = nplain; b < nb0; ++b) {
-        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-#pragma unroll
-        for (std::uint32_t e = 0; e < DPB; ++e) elem(x, b, e, true);
-      }
+    };
+    auto phase_a = [&](auto bern_c, auto wpb_c) {
+      for (std::uint32_t b = 0; b < nplain; ++b) block(b, false, bern_c, wpb_c);
+      for (std::uint32_t b = nplain; b < nb0; ++b) block(b, true, bern_c, wpb_c);
     };
     if (h.pert_mode != 0)
-      phase_a(std::true_type{});
+      phase_a(std::true_type{}, std::integral_constant<std::uint32_t, 0>{});
+    else if (k == 16)
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 2>{});
+    else if (k == 8)
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 1>{});
     else
-      phase_a(std::false_type{});
-
+      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 0>{});
   };
 
   // Function phase of step `sp` (engine.hpp:270-311): the reference's group
@@ -301,16 +315,18 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   auto fn_phase = [&](const std::uint32_t* Sc, std::uint32_t* Sn, const step_philox& sp) {
     for (std::uint32_t w = 0; w < sw32; ++w) Sn[32 * w] = 0;
     uint4 xb = make_uint4(0, 0, 0, 0);  // the phase-B block holding draw j
+    // r53 of draw j = gi for the rare FP64 path: high word + the low block's word
+    auto r53_of = [&](std::uint32_t gi, const raw53& r) -> std::uint64_t {
+      return raw53{r.hi, lo_word<STREAM>(sp, nb0 + gi / DPB, gi % DPB, rp.rk0, rp.rk1)}.value();
+    };
     for (std::uint32_t gi = 0; gi < NG; ++gi) {
       raw53 r{0, 0};
       std::uint32_t r32 = 0;
       if (gi < A) {  // draw j = gi (alias groups come first)
         const std::uint32_t e = gi % DPB;
         if (e == 0) xb = philox_block(sp, nb0 + gi / DPB, rp.rk0, rp.rk1);
-        if constexpr (STREAM == STREAM_U53)
-          r = pick53(xb, e);
-        else
-          r32 = pick32(xb, e);
+        r.hi = pick32(xb, e);
+        r32 = r.hi;
       }
       std::uint32_t olo, ohi = 0, off, members;
       if (gi < A1) {  // single node at offset gi, inline 1-bit tables (dev_plan.h arec)
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
         // tail of compact plans (global memory; ldp<false> is then generic)
         std::uint32_t f = base + alias_fast(acell_s, asz, base, r, r32, rare);
         if constexpr (STREAM == STREAM_U53)
-          if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r.value());
+          if (__builtin_expect(rare, 0)) f = base + alias_exact_fp64(acut, aidx, asz, base, r53_of(gi, r));
         const uint4 F = ldp<GC>(fns_s + f);
         olo = (F.x >> gather_fn(Sc, F)) & 1u;
         off = gi;
@@ -336,7 +352,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
           bool rare = exact_all || (G.w & kGroupExactAlias);
           idx = alias_fast(acell, asz, G.z, r, r32, rare);
           if constexpr (STREAM == STREAM_U53)
-            if (__builtin_expect(rare, 0)) idx = alias_exact_fp64(acut, aidx, asz, G.z + h.cell_base, r.value());
+            if (__builtin_expect(rare, 0)) idx = alias_exact_fp64(acut, aidx, asz, G.z + h.cell_base, r53_of(gi, r));
         }
         const uint4 F = ldp<GC>(fns + G.y + idx);
         const std::uint32_t v = gather_fn(Sc, F);

@@ -1,7 +1,8 @@
 // Philox4x32-10 for the trajectory kernels (Salmon et al., SC'11).
 //
 // Counter layout: c = (trajectory, draw block,
-// step lo32, step hi32), key = seed. Within one step only the draw block
+// step lo32, step hi32), key = seed; U53 low words come from the blocks
+// b | kLoBlock. Within one step only the draw block
 // changes, so the first round is two XORs and the second round one 32x32
 // multiply: `step_philox` carries the block-independent parts, computed once
 // per step, and `block()` runs the remaining ~8.5 rounds.
@@ -13,6 +14,12 @@ namespace pbn_b200 {
 
 constexpr std::uint32_t kPhiloxM0 = 0xD2511F53u;
 constexpr std::uint32_t kPhiloxM1 = 0xCD9E8D57u;
+// U53 draws are split over two blocks: draw e of block b takes
+// its high word from block b and its low word from block b | kLoBlock. Every
+// decision of the kernels is made by the high word alone except on a tie
+// (about 2^-16 of perturbation draws at k = 16, ~N * 2^-32 of selections), so
+// the low blocks are computed only in those rare paths.
+constexpr std::uint32_t kLoBlock = 0x80000000u;
 
 struct step_philox {
   std::uint32_t a;   // hi(M1*step_lo) ^ k0[0]        -> round-1 c0 = a ^ block

@@ -46,12 +46,14 @@ def test_philox_matches_curand_host_generator(orc):
 
 
 def test_stream_layout(orc):
-    """draw d: phase A (d <= g) in block d/DPB; phase B starts on block
-    ceil((g+1)/DPB) (DESIGN.md "Random stream")."""
+    """draw d: phase A (d <= g) at block position d/4, word d%4; phase B starts
+    on block position ceil((g+1)/4). U53 takes its high word from block b and
+    its low word from block b | 2^31."""
     seed, traj, step = 77, 5, 123
     key = [seed, 0]
-    for g in (1, 4, 7, 12):
-        for kind, dpb in ((0, 2), (1, 4)):
+    dpb = 4
+    for g in (1, 4, 7, 12, 63):
+        for kind in (0, 1):
             nb0 = (g + 1 + dpb - 1) // dpb
             for d in range(g + 1 + 3 * dpb):
                 if d <= g:
@@ -60,7 +62,8 @@ def test_stream_layout(orc):
                     b, e = nb0 + (d - g - 1) // dpb, (d - g - 1) % dpb
                 x = orc.philox([traj, b, step, 0], key)
                 if kind == 0:
-                    want = ((int(x[2 * e + 1]) << 32 | int(x[2 * e])) >> 11) * 2.0**-53
+                    y = orc.philox([traj, b | 0x80000000, step, 0], key)
+                    want = ((int(x[e]) << 32 | int(y[e])) >> 11) * 2.0**-53
                 else:
                     want = int(x[e]) * 2.0**-32
                 assert orc.draw(seed, traj, step, d, kind, g) == want
