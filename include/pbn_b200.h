@@ -347,6 +347,12 @@ double pbn_inverse_normal_cdf(double p);
 uint32_t pbn_internal_lower_bound(const uint32_t* w, uint32_t n, uint64_t theta);
 int pbn_internal_greedy_partition(const uint32_t* w, uint32_t n, uint32_t m, uint32_t* part_of);
 int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint32_t* alias);
+/* Device encoding of a plan without a device (test / sizing hook): out[] =
+ * section offsets pert53, pert32, groups, fns, grec, acut, aidx, acell, arec,
+ * scol, arec4, tables, fns_s, acell_s, then core_bytes, table_bytes,
+ * blob_bytes (stageable), total bytes, A, A1, groups, sw32, rg_ok,
+ * single_compact (first n_out of them). */
+int pbn_internal_plan_layout(const pbn_plan_view* view, uint64_t* out, uint32_t n_out);
 /* Integer form of the U53 combined-function choice (dev_plan.h a53) evaluated on
  * the host exactly as the kernel does it, fast path and boundary fallback, for
  * raw draw words R[i] = x[2e+1] << 32 | x[2e]; n <= 2048. Test hook. */

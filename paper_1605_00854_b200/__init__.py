@@ -197,6 +197,7 @@ def _load():
         "pbn_group_run": (I, [P, C.POINTER(RunArgs), C.POINTER(U64), C.POINTER(U64),
                               C.POINTER(U64), C.POINTER(U64)]),
         "pbn_group_destroy": (None, [P]),
+        "pbn_internal_plan_layout": (I, [C.POINTER(PlanView), C.POINTER(U64), U32]),
         "pbn_internal_lower_bound": (U32, [C.POINTER(U32), U32, U64]),
         "pbn_internal_greedy_partition": (I, [C.POINTER(U32), U32, U32, C.POINTER(U32)]),
         "pbn_internal_alias_build": (I, [C.POINTER(C.c_double), U32, C.POINTER(C.c_double),
@@ -421,6 +422,21 @@ def prepare(model: Model, theta=DEFAULT_THETA, k_max=DEFAULT_K, max_group_parent
     h = C.c_void_p()
     _check(lib.pbn_prepare(model._h, theta, k_max, max_group_parents, C.byref(h)))
     return PreparedSimulation(h.value, model, theta, k_max, max_group_parents)
+
+
+PLAN_LAYOUT_FIELDS = ("off_pert53", "off_pert32", "off_groups", "off_fns", "off_grec", "off_acut",
+                      "off_aidx", "off_acell", "off_arec", "off_scol", "off_arec4", "off_tables",
+                      "off_fns_s", "off_acell_s", "core_bytes", "table_bytes", "blob_bytes",
+                      "total_bytes", "n_alias_groups", "n_single_alias", "n_groups", "sw32",
+                      "rg_ok", "single_compact")
+
+
+def plan_layout(plan) -> dict:
+    """Device encoding sizes/offsets of a plan (no device needed)."""
+    out = np.zeros(len(PLAN_LAYOUT_FIELDS), np.uint64)
+    view = plan.view if isinstance(plan, PreparedSimulation) else plan
+    _check(lib.pbn_internal_plan_layout(C.byref(view), _u64p(out), len(out)))
+    return {k: int(v) for k, v in zip(PLAN_LAYOUT_FIELDS, out)}
 
 
 def lower_bound(weights, theta):

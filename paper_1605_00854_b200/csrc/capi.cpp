@@ -768,6 +768,22 @@ int pbn_internal_alias_build(const double* probs, uint32_t n, double* cut, uint3
   });
 }
 
+int pbn_internal_plan_layout(const pbn_plan_view* view, uint64_t* out, uint32_t n_out) {
+  return guard([&] {
+    need(view, "view");
+    need(out, "out");
+    check_view(*view);
+    const encoded_plan ep = encode_plan(*view);
+    const dev_plan_header& h = ep.h;
+    const uint64_t v[] = {h.off_pert53, h.off_pert32, h.off_groups, h.off_fns, h.off_grec,
+                          h.off_acut, h.off_aidx, h.off_acell, h.off_arec, h.off_scol,
+                          h.off_arec4, h.off_tables, h.off_fns_s, h.off_acell_s, h.core_bytes,
+                          h.table_bytes, h.blob_bytes, ep.blob.size(), h.n_alias_groups,
+                          h.n_single_alias, h.n_groups, h.sw32, h.rg_ok, h.single_compact};
+    for (uint32_t i = 0; i < n_out && i < sizeof(v) / sizeof(v[0]); ++i) out[i] = v[i];
+  });
+}
+
 int pbn_internal_alias53_pick(const double* cut, const uint32_t* alias, uint32_t n,
                               const uint64_t* raw, uint64_t m, uint32_t* pick,
                               uint8_t* took_fast) {
