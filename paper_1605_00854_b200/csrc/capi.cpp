@@ -32,7 +32,7 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
                                  std::uint64_t* d_counts, cudaStream_t stream,
                                  std::uint32_t* launches);
 bool lane_kernel_fits(const dev_plan_header& h);
-int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt);
+int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
 std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
@@ -194,7 +194,7 @@ int next_lower_place(int place) {
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
 std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt,
-                         bool node_counts) {
+                         bool node_counts, std::uint32_t min_staged = 0) {
   if (lpt == 1 && lane_kernel_fits(g.ep.h)) {  // lane kernel: 32 trajectories per warp
     const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) + 31) / 32;
     std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
@@ -211,7 +211,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
   const std::uint64_t stride =
       (2 * g.ep.h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
-  const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
+  const std::uint64_t avail = g.smem_optin - std::max(staged_bytes(g), min_staged) - 64;
   while (w > 1 && w * per_warp > avail) --w;
   if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
   return static_cast<std::uint32_t>(w);
@@ -279,14 +279,18 @@ struct launch_choice {
   int gm = 0;
 };
 
-launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc) {
+launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, std::uint32_t stream) {
   pbn_gpu& g = const_cast<pbn_gpu&>(g0);  // pick_warps reads g.place; restored below
   launch_choice c;
   c.lpt = g.lpt_fixed ? g.lpt_fixed : auto_lpt(g.ep.h.n_kept, n_traj, g.sms);
+  c.lane = c.lpt == 1 && lane_kernel_fits(g.ep.h);
+  c.gm = c.lane ? -1 : ensemble_gather_mode(g.ep.h, c.lpt, static_cast<int>(stream));
+  // GM 4 kernels stage the compact single-node group records at any placement
+  const std::uint32_t min_staged = c.gm == 4 ? g.ep.h.off_sfn : 0u;
   const int place0 = g.place;
   for (;;) {
     try {
-      c.warps = pick_warps(g, n_traj, c.lpt, nc);
+      c.warps = pick_warps(g, n_traj, c.lpt, nc, min_staged);
       break;
     } catch (const resource_error&) {
       if (g.place == 0) {
@@ -298,15 +302,13 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc) {
   }
   c.place = g.place;
   g.place = place0;
-  c.lane = c.lpt == 1 && lane_kernel_fits(g.ep.h);
   c.scan = c.lane && g.p_fn < kScanBelow;
-  c.gm = c.lane ? -1 : ensemble_gather_mode(g.ep.h, c.lpt);
   return c;
 }
 
 std::string kernel_name(const launch_choice& c, std::uint32_t stream) {
   static const char* places[] = {"global", "core", "tables", "all", "core_pert"};
-  static const char* gms[] = {"smem", "shfl", "shfl_compact", "shfl2"};
+  static const char* gms[] = {"smem", "shfl", "shfl_compact", "shfl2", "smem_compact"};
   std::string s = c.lane ? std::string("lane<") + (c.scan ? "scan" : "lockstep")
                          : "subwarp<lpt=" + std::to_string(c.lpt) + ",gather=" + gms[c.gm];
   s += std::string(",stream=") + (stream == PBN_STREAM_U53 ? "u53" : "u32");
@@ -322,7 +324,7 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
   if (nc && !d_node_counts) throw std::invalid_argument("PBN_RUN_NODE_COUNTS needs node_counts");
   rp.node_counts = nc ? d_node_counts : nullptr;
   ck(cudaSetDevice(g.device), "cudaSetDevice");
-  const launch_choice c = choose_launch(g, a.n_traj, nc);
+  const launch_choice c = choose_launch(g, a.n_traj, nc, a.stream);
 
   g.last_lpt = c.lpt;
   g.last_warps = c.warps;
@@ -715,7 +717,7 @@ int pbn_gpu_plan_launch(const pbn_gpu* g, uint32_t n_traj, uint32_t stream, uint
                         char* buf, size_t cap, size_t* len_out) {
   return guard([&] {
     need(g, "gpu");
-    const launch_choice c = choose_launch(*g, n_traj, (flags & PBN_RUN_NODE_COUNTS) != 0);
+    const launch_choice c = choose_launch(*g, n_traj, (flags & PBN_RUN_NODE_COUNTS) != 0, stream);
     copy_str(kernel_name(c, stream), buf, cap, len_out);
   });
 }

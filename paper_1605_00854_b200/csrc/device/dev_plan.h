@@ -57,6 +57,16 @@
 //   tables        packed member outputs, entry width 1/2/4/8 bytes by member count
 //   acut[A] f64, aidx[A] u32 (exact section): the group cut-offs and targets
 //                      for the FP64 path (boundary draws, groups with N > 2048)
+//   sgrp[A1]      uint4 (single_compact_l, n' > 2047) per single-node alias group
+//                      j (N <= 4 functions): U53 cell c in word c = hi32(C[c]) with
+//                      bits [0, 4) replaced by alias[c] << 2 | (c == 0 ? N-1 : 0);
+//                      a draw's high word hi picks e = (hi * N) >> 32 and then
+//                      e if hi >> 4 < word_e >> 4, alias if greater — equal, or
+//                      (hi * N mod 2^32) > ~N, is rare (exact redo). First
+//                      section, staged by every GM 4 launch.
+//   sfn[4 A1]     uint4 (single_compact_l) function c of group j at 4j + c:
+//                      {1-bit table of <= 32 entries, records 0 | 1 << 16,
+//                      records 2 | 3 << 16, record 4 | gather count << 16}
 //   fns_s, acell_s     (single_compact) the single-node groups' fns and acell
 //                      entries, moved out of the staged core: the compact kernels
 //                      read scol instead; fallback kernels (other LPT) read these
@@ -120,6 +130,8 @@ struct dev_plan_header {
   std::uint32_t rg_ok;           // sw32 <= 32: one state word per lane fits a warp (SHFL gather)
   std::uint32_t single_gc5;      // some function of groups [0, A1) has 5 parents
   std::uint32_t single_compact;  // rg_ok, A1 >= 32, no 5-parent function: sfn/arec4 present
+  std::uint32_t single_compact_l;  // !rg_ok, A1 >= 32, every single group N <= 4: sgrp/sfn present
+  std::uint32_t off_sgrp, off_sfn;  // sgrp at 0: the GM 4 kernels stage [0, off_sfn)
   std::uint32_t pert_mode;       // 0 grouped patterns, 1 per-node Bernoulli(p) (Method_old)
   std::uint32_t has_leaf;        // phase A ends with the leaf draw
   std::uint64_t pthr53;          // Bernoulli: flip iff R < ceil(p * 2^53) << 11 (raw word)

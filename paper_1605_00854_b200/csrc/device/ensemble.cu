@@ -22,6 +22,7 @@
 //     stream starts phase B on a fresh Philox block.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -61,11 +62,16 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   constexpr bool GT = placement<PLACE>::global_tables;  // tables read from global
   constexpr bool GP = placement<PLACE>::global_pert;    // perturbation cells read from global
   constexpr std::uint32_t DPB = draws<STREAM>::kPerBlock;
-  constexpr bool RG = GM >= 1;
+  constexpr bool RG = GM >= 1 && GM <= 3;
   constexpr bool RG2 = GM == 3;
   constexpr bool SC = GM == 2;
+  constexpr bool SCL = GM == 4;  // compact single-node records, shared-memory gathers (n' > 2047)
 
-  const std::uint32_t staged = stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
+  // GM 4 stages at least the sgrp section (blob bytes [0, off_sfn))
+  const std::uint32_t staged =
+      SCL && staged_prefix<STREAM>(h, PLACE) < h.off_sfn
+          ? (stage_plan(smem, gblob, h.off_sfn, &stage_bar), h.off_sfn)
+          : stage_placement<STREAM, PLACE>(smem, gblob, h, &stage_bar);
 
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
@@ -86,6 +92,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const uint4* acell_s = reinterpret_cast<const uint4*>(sbase + h.off_acell_s);
   const std::uint32_t* arec = reinterpret_cast<const std::uint32_t*>(core + h.off_arec);
   const uint4* arec4 = reinterpret_cast<const uint4*>(core + h.off_arec4);
+  const uint4* sgrp = reinterpret_cast<const uint4*>(smem + h.off_sgrp);  // GM 4: always staged
+  const uint4* sfn = reinterpret_cast<const uint4*>(core + h.off_sfn);
 
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t r = lane % LPT;
@@ -324,7 +332,18 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // loads and shuffles only, so two groups can be interleaved by the scheduler.
   auto single_fn = [&](std::uint32_t j, std::uint32_t jj, bool& rare) -> std::uint32_t {
     rare = false;
-    if constexpr (SC) {
+    if constexpr (SCL) {
+      // sgrp cells (dev_plan.h): the choice on the high word's top 28 bits
+      const uint4 R = sgrp[j];
+      const std::uint32_t hi = dbuf[jj];
+      const std::uint32_t N = (R.x & 3u) + 1u;
+      const std::uint64_t P = static_cast<std::uint64_t>(hi) * N;
+      const std::uint32_t e = static_cast<std::uint32_t>(P >> 32);
+      const std::uint32_t cell = e == 0 ? R.x : e == 1 ? R.y : e == 2 ? R.z : R.w;
+      const std::uint32_t hT = hi >> 4, cT = cell >> 4;
+      rare = static_cast<std::uint32_t>(P) > ~N || hT == cT;
+      return 4 * j + (hT < cT ? e : (cell >> 2) & 3u);
+    } else if constexpr (SC) {
       const uint4 ar = ldp<GC>(arec4 + j);  // {U53 cell offset, function offset, N, ~N}
       std::uint32_t pick;
       if constexpr (STREAM == STREAM_U53) {
@@ -352,7 +371,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     }
   };
   auto single_out = [&](const std::uint32_t* Sc, std::uint32_t wreg, std::uint32_t f) -> bool {
-    if constexpr (SC) {
+    if constexpr (SCL) {
+      // five 16-bit records from the shared state (unused slots read bit n')
+      const uint4 F = ldp<GC>(sfn + f);
+      const std::uint32_t w4 = Sc[(F.w & 0xFFFFu) >> 5];
+      const std::uint32_t v = gather4(Sc, F.y, F.z, 0) | (__funnelshift_r(w4, w4, F.w) & 16u);
+      return (F.x >> v) & 1u;
+    } else if constexpr (SC) {
       // compact record: 10-bit records (word << 5 | rotation), table at bits 16..31
       const uint2 F = ldp<GC>(reinterpret_cast<const uint2*>(core + f));
       const std::uint32_t w0 = __shfl_sync(0xFFFFFFFFu, wreg, F.x >> 5);
@@ -651,7 +676,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           __syncwarp(smask);
         }
         jstart = jfull;
-      } else if constexpr (SC && DPB * CB == 4 && kQuadRounds && !kPhiloxPipeline) {
+      } else if constexpr ((SC || SCL) && DPB * CB == 4 && kQuadRounds && !kPhiloxPipeline) {
         // U32 compact: chunks of one single-node quad
         const std::uint32_t jfull = A1 & ~(4u * LPT - 1u);
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 4 * LPT) {
@@ -684,7 +709,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         for (std::uint32_t t = 0; t < DPB * CB; t += 2) {
           const std::uint32_t jr0 = j0 + t * LPT, jr1 = jr0 + LPT;
           if (jr0 >= A) break;
-          if constexpr (kQuadRounds && SC && DPB * CB >= 4) {
+          if constexpr (kQuadRounds && (SC || SCL) && DPB * CB >= 4) {
             // four single-node rounds at once: four independent chains
             if ((t & 3) == 0 && jr0 + 4 * LPT <= A1) {
               single_quad(Sc, Sn, wreg, jr0, t);
@@ -932,6 +957,8 @@ kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
     case 16:
       return pick_place<16, STREAM, 0>(place);
     default:
+      if constexpr (STREAM == STREAM_U53)
+        if (gm == 4) return pick_place<32, STREAM, 4>(place);
       return gm == 3   ? pick_place<32, STREAM, 3>(place)
              : gm == 2 ? pick_place<32, STREAM, 2>(place)
              : gm == 1 ? pick_place<32, STREAM, 1>(place)
@@ -954,9 +981,13 @@ std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_co
 // shuffles; with the compact single-node records (SC) when the plan has them;
 // two words per lane (RG2) only for the single-node rounds (general rounds
 // keep the shared-memory gather: two shuffles per parent lose to it).
-int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt) {
+// GM 4 (U53, n' > 2047): the compact sgrp/sfn single-node records with
+// shared-memory gathers.
+int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream) {
   const bool rg = lpt == 32 && h.rg_ok;
   const bool rg2 = lpt == 32 && !h.rg_ok && h.sw32 <= 64 && h.n_single_alias >= 32 && kUseRg2;
+  if (!rg && !rg2 && lpt == 32 && h.single_compact_l && stream == STREAM_U53 && kUseCompactSingle)
+    return 4;
   return rg2 ? 3 : !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
 }
 
@@ -965,13 +996,14 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches) {
-  const int gm = ensemble_gather_mode(h, lpt);
+  const int gm = ensemble_gather_mode(h, lpt, stream_kind);
   const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm);
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;
-  const std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
-                                                      : staged_prefix<STREAM_U32>(h, place);
+  std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
+                                                : staged_prefix<STREAM_U32>(h, place);
+  if (gm == 4) staged = std::max<std::size_t>(staged, h.off_sfn);
   const std::size_t smem =
       staged + static_cast<std::size_t>(slots) * slot_words(h, lpt, rp.node_counts != nullptr) * 4 + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),

@@ -391,6 +391,42 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
     }
   }
 
+  // Compact single-node records for networks too large for the register
+  // gather (n' > 2047: the sub-warp kernel's shared-memory gather, GM 4;
+  // dev_plan.h sgrp/sfn): sgrp[j] = the group's N <= 4 U53 cells, one word
+  // each: hi32(C[c]) with the low 4 bits replaced by alias[c] << 2 (and N-1
+  // in cell 0) — the kernel compares the high word's top 28 bits, a tie
+  // being rare (redo); sfn[4j + c] = {1-bit inline table, records 0|1,
+  // records 2|3, record 4 | gather count << 16} (16-bit records, as fns).
+  h.single_compact_l = !h.single_compact && h.sw32 > 64 && h.n_single_alias >= 32 && n < 65536 ? 1u : 0u;
+  for (std::uint32_t gi = 0; h.single_compact_l && gi < h.n_single_alias; ++gi)
+    if (v.grp_alias_size[gi] > 4) h.single_compact_l = 0;
+  std::vector<std::uint32_t> sgrp, sfn;
+  if (h.single_compact_l) {
+    const std::uint32_t A1 = h.n_single_alias;
+    sgrp.assign(4 * static_cast<std::size_t>(A1), 0);
+    sfn.assign(16 * static_cast<std::size_t>(A1), 0);
+    for (std::uint32_t gi = 0; gi < A1; ++gi) {
+      const std::uint32_t asz = v.grp_alias_size[gi], ab = v.grp_alias_begin[gi];
+      for (std::uint32_t c = 0; c < asz; ++c) {
+        const std::uint32_t al = acell[4 * (ab + c) + 0], hi = acell[4 * (ab + c) + 1];
+        if (al >= asz) throw model_error("alias target out of range");
+        sgrp[4 * gi + c] = (hi & ~0xFu) | (al << 2) | (c == 0 ? asz - 1 : 0u);
+        const std::uint32_t f = v.grp_fn_begin[gi] + c;
+        const std::uint32_t gc = v.fn_gather_count[f];
+        if (gc > 5 || fn_members[f] != 1) throw model_error("compact single-node record misuse");
+        std::uint32_t table = 0;
+        for (std::uint32_t e = 0; e < (1u << gc); ++e)
+          table |= static_cast<std::uint32_t>(v.fn_tables[v.fn_table_begin[f] + e] & 1u) << e;
+        std::uint32_t* F = &sfn[16 * static_cast<std::size_t>(gi) + 4 * c];
+        F[0] = table;
+        F[1] = record(f, 0) | (static_cast<std::uint32_t>(record(f, 1)) << 16);
+        F[2] = record(f, 2) | (static_cast<std::uint32_t>(record(f, 3)) << 16);
+        F[3] = record(f, 4) | (gc << 16);
+      }
+    }
+  }
+
   // With the compact records the single-node groups' fns/acell entries are
   // needed only by the fallback (non-compact) kernels: they move to an
   // unstaged tail (fns_s, acell_s) and the staged fns/acell start at the first
@@ -431,6 +467,8 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   };
   // placement prefixes: [core | tables | pert32 | pert53] — a launch stages
   // the longest prefix that fits in shared memory and reads the rest via L1/L2
+  h.off_sgrp = section(4 * sgrp.size());  // 0: staged by every GM 4 launch
+  h.off_sfn = section(4 * sfn.size());
   h.off_groups = section(4 * groups.size());
   h.off_fns = section(4 * fns.size());
   h.off_grec = section(2 * grec.size());
@@ -457,6 +495,8 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   if (off > 0xFFFFFFF0ull) throw resource_error("device plan exceeds 4 GiB");
   ep.total_bytes = static_cast<std::uint32_t>(off);
   ep.blob.assign(off, 0);
+  put(ep.blob, h.off_sgrp, sgrp);
+  put(ep.blob, h.off_sfn, sfn);
   put(ep.blob, h.off_pert53, pert53);
   put(ep.blob, h.off_pert32, pert32);
   put(ep.blob, h.off_groups, groups);

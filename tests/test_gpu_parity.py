@@ -25,6 +25,9 @@ CASES = {
     # 1023 < n' <= 2047 with 5-parent functions: two state words per lane (RG2)
     "p5w": (1500, (1, 3), (1, 5), 0.001, 0.0, 2, False, 12, 12, 8),
     "c4": (5000, (1, 4), (1, 5), 0.0001, 0.0, 2, False, 1608, 12, 12),
+    # n' > 2047 with single-node groups of <= 4 functions: the compact
+    # shared-memory-gather records (GM 4, dev_plan.h sgrp/sfn)
+    "big_scl": (2600, (1, 4), (1, 5), 0.0002, 0.0, 2, False, 21, 16, 8),
 }
 
 
@@ -40,7 +43,8 @@ def cuda_ok(pb):
     assert pb.device_count() >= 1, "no CUDA device visible"
 
 
-@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16", "c5_k16", "p5", "p5w", "c4"])
+@pytest.mark.parametrize("case", ["c1", "c3", "c2", "c5", "c1_k16", "c5_k16", "p5", "p5w", "c4",
+                                  "big_scl"])
 @pytest.mark.parametrize("stream", [0, 1])
 def test_bit_exact_vs_oracle(pb, orc, cuda_ok, case, stream):
     plan, pred = _setup(pb, case)
@@ -214,3 +218,24 @@ def test_word_phase_a_any_lanes_per_trajectory(pb, orc, cuda_ok, lpt, stream):
     st, cnt = eng.simulate(seed=21, n_traj=90, n_steps=800, pred=pred, stream=stream)
     ost, ocnt = orc.simulate(plan.view, 21, 0, 90, 800, pred=pred, stream=stream)
     assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+
+
+@pytest.mark.parametrize("case", ["big_scl", "c4"])
+def test_compact_large_network_kernel(pb, orc, cuda_ok, case):
+    """GM 4 (compact sgrp/sfn records, shared-memory gathers) is the U53
+    kernel for these plans; bit-exact with the fast path, the forced FP64
+    path (every function phase redone exactly) and on U32 (GM 0)."""
+    plan, pred = _setup(pb, case)
+    assert pb.plan_layout(plan)["single_compact"] == 0
+    eng = pb.GpuEnsemble(plan)
+    n_traj, n_steps = (64, 120)
+    for stream, exact in ((0, False), (0, True), (1, False)):
+        st, cnt = eng.simulate(seed=9, n_traj=n_traj, n_steps=n_steps, pred=pred, stream=stream,
+                               exact_alias=exact, traj_begin=77, step_begin=1000)
+        gm = "smem_compact" if stream == 0 else "smem"
+        assert f"gather={gm}," in eng.last_kernel(), eng.last_kernel()
+        ost, ocnt = orc.simulate(plan.view, 9, 77, n_traj, n_steps, pred=pred, stream=stream,
+                                 step_begin=1000)
+        assert np.array_equal(cnt, ocnt)
+        assert np.array_equal(st, ost)
+        assert cnt[:, 6].sum() > 0  # function phases ran
