@@ -45,6 +45,11 @@ __device__ __noinline__ std::uint32_t alias_exact_fp64(const double* __restrict_
 }
 
 constexpr int kLaneMaxWarps = 28;  // 896 threads: 72 registers per thread
+#ifndef PBN_SCAN_FN_LANES
+#define PBN_SCAN_FN_LANES 28
+#endif
+// SCAN: pending function phases a warp collects before running them
+constexpr int kScanFnLanes = PBN_SCAN_FN_LANES;
 
 // SCAN: lanes scan their own steps through phase A up to the next function
 // phase (pays when the function phase is rare, c1); otherwise all lanes take
@@ -391,31 +396,40 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     // through phase A until one needs the function phase, so the warp runs
     // the (expensive, per-lane) function phase with every lane that still has
     // steps, instead of with the ~(1-p)^n' share whose current step needs it.
+    // One phase-A round at a time: lanes without a pending function phase
+    // advance one step; the warp runs the function phase once at least
+    // kScanFnLanes lanes have one pending (or no lane can scan further), so
+    // neither the scan rounds nor the function phases run with few lanes.
     std::uint64_t s = rp.step_begin;
+    bool need = false;
+    step_philox sp{};
     for (;;) {
-      bool need = false;
-      step_philox sp{};
-      while (s < s_end) {
+      if (!need && s < s_end) {
         sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
         bool flip, leaf;
         std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
         phase_a_step(Sc, sp, flip, leaf);
         if (!flip && !leaf) {
           need = true;
-          break;
+        } else {
+          npert += flip ? 1u : 0u;
+          step_stats(Sc, s);
+          ++s;
         }
-        npert += flip ? 1u : 0u;
-        step_stats(Sc, s);
-        ++s;
       }
-      if (!__any_sync(lmask, need)) break;
-      if (need) {
-        std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
-        fn_phase(wbuf + cur * (sw32 * 32), Sn, sp);
-        cur ^= 1;
-        ++nfn;
-        step_stats(Sn, s);
-        ++s;
+      const std::uint32_t pend = __ballot_sync(lmask, need);
+      const std::uint32_t scanning = __ballot_sync(lmask, !need && s < s_end);
+      if (pend == 0 && scanning == 0) break;
+      if (scanning == 0 || __popc(pend) >= kScanFnLanes) {
+        if (need) {
+          std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
+          fn_phase(wbuf + cur * (sw32 * 32), Sn, sp);
+          cur ^= 1;
+          ++nfn;
+          step_stats(Sn, s);
+          ++s;
+          need = false;
+        }
       }
     }
   } else {

@@ -41,3 +41,31 @@ def test_reference_arm_line():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "1")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_gpus_flag_launches_one_rank_per_gpu(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks
+    through torch.distributed.run on 127.0.0.1 (the driver's own launch);
+    under torchrun, WORLD_SIZE must match --gpus."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    seen = {}
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    a = bench.parse()
+    with pytest.raises(SystemExit):
+        bench.launch_ranks(a)
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:]
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    with pytest.raises(SystemExit):
+        bench.launch_ranks(a)  # WORLD_SIZE 2 != --gpus 4
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    assert bench.launch_ranks(a) is False
+    monkeypatch.delenv("WORLD_SIZE")
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    assert bench.launch_ranks(bench.parse()) is False  # N = 1: no re-launch

@@ -20,6 +20,16 @@ def test_committed_text_is_the_generator_output(pb, name):
     from paper_1605_00854_b200.configs import CONFIGS
 
     w = CONFIGS[name]
+    if bench.WORKLOADS[name].get("generator") == "reference":
+        import oracle
+
+        if not os.path.exists(oracle.REF_SO):
+            pytest.skip("oracle/_ref not built")
+        sys.path.insert(0, os.path.join(ROOT, "workloads"))
+        from make_workloads import reference_text
+
+        assert bench.workload_text(name) == reference_text(bench.WORKLOADS[name])
+        return
     model, terms = w.model()
     assert bench.workload_text(name) == model.serialize()
     assert [list(t) for t in terms] == bench.WORKLOADS[name]["terms"]
