@@ -542,9 +542,11 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // nv samples, np1 with prev = 1, nh1 with hit = 1, n11 with both
   // (n10 = np1 - n11, n01 = nh1 - n11, n00 = nv - np1 - nh1 + n11)
   std::uint32_t nv = 0, np1 = 0, nh1 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
-  std::uint32_t* ser = rp.series ? rp.series + tloc * rp.series_stride : nullptr;
+  // (the series row is recomputed where used: a pointer kept live across the
+  // step loop costs registers the hot loops need)
   std::uint32_t sword = 0;   // series bits of the current word (lane r == 0)
-  if (ser && r == 0 && rp.series_init && rp.series_bit0 > 0 && z0) {
+  if (rp.series != nullptr && r == 0 && rp.series_init && rp.series_bit0 > 0 && z0) {
+    std::uint32_t* ser = rp.series + tloc * rp.series_stride;
     const std::uint64_t p0 = rp.series_bit0 - 1;
     ser[p0 >> 5] |= 1u << (p0 & 31);
   }
@@ -812,7 +814,8 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       }
       if (++nc_pending == 255) nc_flush();
     }
-    if (ser != nullptr && r == 0) {  // launch-uniform branch
+    if (rp.series != nullptr && r == 0) {  // launch-uniform test, then lane 0
+      std::uint32_t* ser = rp.series + tloc * rp.series_stride;
       const std::uint64_t pos = rp.series_bit0 + (s - rp.step_begin);
       sword |= hit << (pos & 31);
       if ((pos & 31) == 31 || s + 1 == s_end) {

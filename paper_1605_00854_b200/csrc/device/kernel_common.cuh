@@ -174,8 +174,10 @@ struct raw53 {
   }
 };
 
+// Word e (0..3) of a block: two levels of selects, no branches.
 __device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e) {
-  return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
+  const std::uint32_t lo = (e & 1u) ? x.y : x.x, hi = (e & 1u) ? x.w : x.z;
+  return (e & 2u) ? hi : lo;
 }
 
 // Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form on
