@@ -541,6 +541,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   // sampled transitions as four sums over samples with a previous sample:
   // nv samples, np1 with prev = 1, nh1 with hit = 1, n11 with both
   // (n10 = np1 - n11, n01 = nh1 - n11, n00 = nv - np1 - nh1 + n11)
+  // The counters are warp-uniform: with LPT >= 8 lane r of the sub-warp
+  // keeps counter r (0 hits, 1 nv, 2 np1, 3 nh1, 4 n11, 5 function-phase
+  // steps, 6 perturbed steps) in one register `cnt`; each step ORs its events
+  // into a bit word and every lane adds its own bit (registers the hot loops
+  // need instead of seven loop-carried counters).
+  constexpr bool LANE_COUNTERS = LPT >= 8;
+  std::uint32_t cnt = 0;
   std::uint32_t nv = 0, np1 = 0, nh1 = 0, n11 = 0, nhit = 0, nfn = 0, npert = 0;
   // (the series row is recomputed where used: a pointer kept live across the
   // step loop costs registers the hot loops need)
@@ -640,9 +647,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     const bool any_flip = __ballot_sync(smask, flip) != 0;
     const bool any_leaf = __ballot_sync(smask, leaf) != 0;
 
+    std::uint32_t ev = 0;  // this step's events (LANE_COUNTERS bit layout)
     if (any_flip) {
       __syncwarp(smask);
-      ++npert;
+      if constexpr (LANE_COUNTERS)
+        ev = 1u << 6;
+      else
+        ++npert;
     } else if (!any_leaf) {
       // ---- function phase, in lockstep rounds of LPT groups
       std::uint32_t* Sn = cur ? S0 : S1;
@@ -786,20 +797,34 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       if constexpr (STREAM == STREAM_U53)
         if (__builtin_expect(__any_sync(smask, rare_acc), 0)) redo_fn_phase(Sc, Sn);
       cur ^= 1;
-      ++nfn;
+      if constexpr (LANE_COUNTERS)
+        ev = 1u << 5;
+      else
+        ++nfn;
     }
 
     // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
     const std::uint32_t hit = pred_eval(cur ? S1 : S0);
-    nhit += hit;
-    if (++kphase == rp.kappa) {
-      kphase = 0;
-      const std::uint32_t valid = (prev >> 1) ^ 1u;  // prev 2 = none
-      nv += valid;
-      np1 += prev & 1u;
-      nh1 += hit & valid;
-      n11 += prev & hit;
-      prev = hit;
+    if constexpr (LANE_COUNTERS) {
+      ev |= hit;
+      if (++kphase == rp.kappa) {
+        kphase = 0;
+        const std::uint32_t valid = (prev >> 1) ^ 1u;  // prev 2 = none
+        ev |= (valid << 1) | ((prev & 1u) << 2) | ((hit & valid) << 3) | ((prev & hit) << 4);
+        prev = hit;
+      }
+      cnt += (ev >> r) & 1u;
+    } else {
+      nhit += hit;
+      if (++kphase == rp.kappa) {
+        kphase = 0;
+        const std::uint32_t valid = (prev >> 1) ^ 1u;  // prev 2 = none
+        nv += valid;
+        np1 += prev & 1u;
+        nh1 += hit & valid;
+        n11 += prev & hit;
+        prev = hit;
+      }
     }
     if (rp.node_counts) {  // launch-uniform branch
       const std::uint32_t* Sf = cur ? S1 : S0;
@@ -832,6 +857,16 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
     const std::uint32_t* Sf = cur ? S1 : S0;
     std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(states + tloc * (sw32 / 2));
     for (std::uint32_t w = r; w < sw32; w += LPT) dst[w] = Sf[w];
+  }
+  if constexpr (LANE_COUNTERS) {
+    const std::uint32_t l0 = (sub * LPT) & 31;
+    nhit = __shfl_sync(smask, cnt, l0 + 0);
+    nv = __shfl_sync(smask, cnt, l0 + 1);
+    np1 = __shfl_sync(smask, cnt, l0 + 2);
+    nh1 = __shfl_sync(smask, cnt, l0 + 3);
+    n11 = __shfl_sync(smask, cnt, l0 + 4);
+    nfn = __shfl_sync(smask, cnt, l0 + 5);
+    npert = __shfl_sync(smask, cnt, l0 + 6);
   }
   if (r == 0) {
     std::uint64_t* c = counts + tloc * 8;
