@@ -158,6 +158,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const std::uint32_t traj = static_cast<std::uint32_t>(rp.traj_begin + tloc);
   std::uint32_t thi0, tlo0;
   mulhilo(kPhiloxM0, traj, thi0, tlo0);
+  // opaque to the compiler: kept in registers rather than rematerialised from
+  // the block/thread ids (S2R + multiply) in every step
+  asm volatile("" : "+r"(thi0), "+r"(tlo0));
 
   // Predicate (engine.hpp:328-332): lane r checks terms r, r+LPT, ...; the
   // sub-warp vote combines them. Called by every lane of the sub-warp.
