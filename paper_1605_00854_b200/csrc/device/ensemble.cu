@@ -607,8 +607,13 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         const std::uint32_t w1 = (c[2] & pam.z) | ((c[3] & pam.w) << 16);
         if (__builtin_expect((w0 | w1) != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
           flip = true;
-          Sc[2 * b] ^= w0;
-          Sc[2 * b + 1] ^= w1;
+          // one 8-byte read-modify-write (words 2b, 2b+1: consecutive lanes
+          // hit consecutive bank pairs; two 4-byte accesses would conflict)
+          uint2* w = reinterpret_cast<uint2*>(Sc) + b;
+          uint2 v = *w;
+          v.x ^= w0;
+          v.y ^= w1;
+          *w = v;
         }
       } else if constexpr (WPB == 1) {  // k = 8: the block's four patterns are word b
         const std::uint32_t w0 = (c[0] & pam.x) | ((c[1] & pam.y) << 8) |
