@@ -122,10 +122,42 @@ int main(int argc, char** argv) {
     hits_total += tr.predicate_hits;
     fn_total += c[PBN_C_FNSTEPS];
   }
+  // the same job through the device group (pbn_group_*):
+  // every device of this box, one ncclAllReduce of the pooled counts
+  int ndev = 0;
+  pbn_device_count(&ndev);
+  pbn::gpu_plan_view pv(ps);
+  pbn_group* grp = nullptr;
+  int grc = pbn_group_create(&pv.v, nullptr, static_cast<std::uint32_t>(ndev), 0, &grp);
+  std::uint32_t group_bad = 0;
+  std::uint64_t group_hits = 0;
+  if (grc == PBN_OK) {
+    std::vector<std::uint64_t> gstates(dev_states.size(), 0), totals(PBN_COUNT_FIELDS, 0);
+    pbn_run_args a{};
+    a.seed = seed;
+    a.n_traj = n_traj;
+    a.stream = PBN_STREAM_U53;
+    a.n_steps = steps;
+    std::vector<std::uint32_t> bits;  // compiled_predicate: (engine bit, value) pairs
+    std::vector<std::uint8_t> vals;
+    for (const auto& [bit, val] : pred) {
+      bits.push_back(bit);
+      vals.push_back(val ? 1 : 0);
+    }
+    a.pred_bits = bits.data();
+    a.pred_vals = vals.data();
+    a.n_pred = static_cast<std::uint32_t>(bits.size());
+    grc = pbn_group_run(grp, &a, gstates.data(), nullptr, totals.data(), nullptr);
+    group_bad = gstates == dev_states ? 0u : 1u;
+    group_hits = totals[PBN_C_HITS];
+    pbn_group_destroy(grp);
+  }
   std::printf("{\"mode\": \"device\", \"trajectories\": %u, \"steps\": %llu, \"n_kept\": %u, "
               "\"state_mismatches\": %u, \"hit_mismatches\": %u, \"hits\": %llu, "
-              "\"fn_phase_steps\": %llu}\n",
+              "\"fn_phase_steps\": %llu, \"group_devices\": %d, \"group_rc\": %d, "
+              "\"group_state_mismatch\": %u, \"group_hits\": %llu}\n",
               n_traj, static_cast<unsigned long long>(steps), ps.kept_count(), bad_states, bad_hits,
-              static_cast<unsigned long long>(hits_total), static_cast<unsigned long long>(fn_total));
-  return bad_states || bad_hits ? 2 : 0;
+              static_cast<unsigned long long>(hits_total), static_cast<unsigned long long>(fn_total),
+              ndev, grc, group_bad, static_cast<unsigned long long>(group_hits));
+  return bad_states || bad_hits || grc != PBN_OK || group_bad || group_hits != hits_total ? 2 : 0;
 }

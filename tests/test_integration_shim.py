@@ -41,7 +41,7 @@ def test_shim_view_accepted_and_leafless_view_refused(pb, tmp_path):
     path, pred = _model_file(pb, tmp_path, 100, (1, 3), (1, 3), 0.01, 0.2, 2, True, 1605)
     out = subprocess.run([shim, path, str(1 << 25), "16", "8", "4", "10", "42", pred,
                           "--no-device"], capture_output=True, text=True, check=True)
-    r = json.loads(out.stdout)
+    r = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert r["create_rc_without_leaf"] == 1  # PBN_EUSAGE, plan never runs
     if pb.device_count() == 0:
         assert r["create_rc"] == 4  # validated + encoded, then no device
@@ -68,8 +68,10 @@ def test_shim_device_equals_reference_simulate(pb, tmp_path, case):
     out = subprocess.run([shim, path, str(1 << 25), str(k), str(mgp), str(n_traj), str(steps),
                           "42", pred], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
-    r = json.loads(out.stdout)
+    r = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert r["state_mismatches"] == 0 and r["hit_mismatches"] == 0
+    # the same job through the C-ABI device group (one ncclAllReduce)
+    assert r["group_rc"] == 0 and r["group_state_mismatch"] == 0 and r["group_hits"] == r["hits"]
     assert r["fn_phase_steps"] > 0
 
 
