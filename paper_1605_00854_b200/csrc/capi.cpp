@@ -35,6 +35,8 @@ bool lane_kernel_fits(const dev_plan_header& h);
 int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
 std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
+const char* lane_rare_fn_name();
+std::size_t lane_cta_bytes();
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
                               std::uint32_t n, cudaStream_t stream);
 cudaError_t launch_series_stats(const std::uint32_t* d_series, std::uint32_t n_traj,
@@ -200,7 +202,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
     std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
     w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lane_max_warps(), w));
     const std::uint64_t per_warp = lane_warp_words(g.ep.h, node_counts) * 4;
-    const std::uint64_t avail = g.smem_optin - staged_bytes(g) - 64;
+    const std::uint64_t avail = g.smem_optin - staged_bytes(g) - lane_cta_bytes() - 64;
     while (w > 1 && w * per_warp > avail) --w;
     if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
     return static_cast<std::uint32_t>(w);
@@ -309,7 +311,7 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, st
 std::string kernel_name(const launch_choice& c, std::uint32_t stream) {
   static const char* places[] = {"global", "core", "tables", "all", "core_pert"};
   static const char* gms[] = {"smem", "shfl", "shfl_compact", "shfl2", "smem_compact"};
-  std::string s = c.lane ? std::string("lane<") + (c.scan ? "scan" : "lockstep")
+  std::string s = c.lane ? std::string("lane<") + (c.scan ? lane_rare_fn_name() : "lockstep")
                          : "subwarp<lpt=" + std::to_string(c.lpt) + ",gather=" + gms[c.gm];
   s += std::string(",stream=") + (stream == PBN_STREAM_U53 ? "u53" : "u32");
   s += std::string(",place=") + places[c.place] + ",warps=" + std::to_string(c.warps) + ">";

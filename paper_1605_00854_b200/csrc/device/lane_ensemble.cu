@@ -55,7 +55,8 @@ constexpr int kScanFnLanes = PBN_SCAN_FN_LANES;
 // phase (pays when the function phase is rare, c1); otherwise all lanes take
 // step s together and the function phase runs under divergence (c3, where
 // ~90% of steps reach it).
-template <int STREAM, int PLACE, bool SCAN>
+// MODE 0 lockstep, 1 scan-ahead (SCAN), 2 CTA-compacted function phases.
+template <int STREAM, int PLACE, int MODE>
 __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     pbn_lane_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                     const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
@@ -88,8 +89,10 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   const std::uint32_t lane = threadIdx.x & 31;
   const std::uint32_t warp = threadIdx.x >> 5;
   const std::uint64_t tloc = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const std::uint32_t lmask = __ballot_sync(0xFFFFFFFFu, tloc < rp.n_traj);  // live lanes
-  if (tloc >= rp.n_traj) return;
+  constexpr bool SCAN = MODE == 1;
+  const bool alive = tloc < rp.n_traj;  // MODE 2 keeps the rest for the CTA barriers
+  const std::uint32_t lmask = __ballot_sync(0xFFFFFFFFu, alive);  // live lanes
+  if (MODE != 2 && !alive) return;
 
   // per-warp shared memory: two state buffers of sw32 words x 32 lanes, then
   // (node counts) 8 counter planes per word; lane columns
@@ -101,7 +104,8 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   std::uint32_t cur = 0;                          // current state buffer (per lane)
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
-    for (std::uint32_t w = 0; w < sw32; ++w) wbuf[32 * w] = src[w] & state_word_mask(h.n_kept, w);
+    for (std::uint32_t w = 0; w < sw32; ++w)
+      wbuf[32 * w] = alive ? src[w] & state_word_mask(h.n_kept, w) : 0u;
     if (rp.node_counts)
       for (std::uint32_t i = 0; i < 8 * sw32; ++i) planes[32 * i] = 0;
   }
@@ -390,7 +394,67 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     }
   };
 
-  if constexpr (SCAN) {
+  if constexpr (MODE == 2) {
+    // CTA-compacted function phases: every trajectory of the CTA advances
+    // one step per iteration; phase A and the statistics run with all lanes,
+    // and the function phases the step needs are packed into a task list
+    // (warp ballots + a prefix over the warps) that the first
+    // ceil(tasks / 32) warps run with full lanes — a thread may run another
+    // lane's trajectory: its state column, its buffer parity and its stream
+    // (seed, trajectory, step) travel with the task.
+    std::uint32_t* cta = reinterpret_cast<std::uint32_t*>(smem + staged) +
+                         static_cast<std::size_t>(blockDim.x >> 5) * warp_words;
+    std::uint32_t* wcnt = cta;                                          // [32]
+    std::uint16_t* task = reinterpret_cast<std::uint16_t*>(cta + 32);  // [blockDim]
+    std::uint32_t* states0 = reinterpret_cast<std::uint32_t*>(smem + staged);
+    const std::uint32_t nwarps = blockDim.x >> 5;
+    const std::uint32_t lt_mask = (1u << lane) - 1u;
+    for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
+      std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
+      bool need = false;
+      if (alive) {
+        const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+        bool flip, leaf;
+        phase_a_step(Sc, sp, flip, leaf);
+        need = !flip && !leaf;
+        if (!need) {
+          npert += flip ? 1u : 0u;
+          step_stats(Sc, s);
+        }
+      }
+      const std::uint32_t bal = __ballot_sync(0xFFFFFFFFu, need);
+      if (lane == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      // exclusive prefix of the warp counts (every warp computes it)
+      std::uint32_t v = lane < nwarps ? wcnt[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= static_cast<std::uint32_t>(o)) v += t;
+      }
+      const std::uint32_t total = __shfl_sync(0xFFFFFFFFu, v, 31);
+      const std::uint32_t before = __shfl_sync(0xFFFFFFFFu, v, warp) - __popc(bal);
+      if (need) task[before + __popc(bal & lt_mask)] =
+          static_cast<std::uint16_t>(threadIdx.x | (cur << 15));
+      __syncthreads();
+      if (threadIdx.x < total) {
+        const std::uint32_t e = task[threadIdx.x];
+        const std::uint32_t q = e & 0x7FFFu, qc = e >> 15;
+        std::uint32_t* col = states0 + static_cast<std::size_t>(q >> 5) * warp_words + (q & 31u);
+        const std::uint32_t tq = static_cast<std::uint32_t>(rp.traj_begin + blockIdx.x * blockDim.x + q);
+        std::uint32_t qh, ql;
+        mulhilo(kPhiloxM0, tq, qh, ql);
+        const step_philox spq = make_step_philox(qh, ql, s, rp.rk0, rp.rk1);
+        fn_phase(col + qc * (sw32 * 32), col + (qc ^ 1u) * (sw32 * 32), spq);
+      }
+      __syncthreads();
+      if (need) {
+        cur ^= 1;
+        ++nfn;
+        step_stats(wbuf + cur * (sw32 * 32), s);
+      }
+    }
+  } else if constexpr (SCAN) {
     // The class of a step (perturbed / leaf no-op / function phase) depends
     // on the stream only, never on the state: each lane scans its own steps
     // through phase A until one needs the function phase, so the warp runs
@@ -450,6 +514,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
       step_stats(Sc, s);
     }
   }
+  if (!alive) return;
   if (rp.node_counts && nc_pending) nc_flush();
   if (rp.tprev) rp.tprev[tloc] = static_cast<std::uint8_t>(prev | (kphase << 2));
   {
@@ -472,21 +537,34 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
 using lane_kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
                                 std::uint64_t*, std::uint64_t*);
 
-template <int STREAM, bool SCAN>
+template <int STREAM, int MODE>
 lane_kernel_fn pick_lane_place(int place) {
   switch (place) {
     case PLACE_ALL:
-      return pbn_lane_kernel<STREAM, PLACE_ALL, SCAN>;
+      return pbn_lane_kernel<STREAM, PLACE_ALL, MODE>;
     case PLACE_CORE_PERT:
-      return pbn_lane_kernel<STREAM, PLACE_CORE_PERT, SCAN>;
+      return pbn_lane_kernel<STREAM, PLACE_CORE_PERT, MODE>;
     case PLACE_TABLES:
-      return pbn_lane_kernel<STREAM, PLACE_TABLES, SCAN>;
+      return pbn_lane_kernel<STREAM, PLACE_TABLES, MODE>;
     case PLACE_CORE:
-      return pbn_lane_kernel<STREAM, PLACE_CORE, SCAN>;
+      return pbn_lane_kernel<STREAM, PLACE_CORE, MODE>;
     default:
-      return pbn_lane_kernel<STREAM, PLACE_GLOBAL, SCAN>;
+      return pbn_lane_kernel<STREAM, PLACE_GLOBAL, MODE>;
   }
 }
+
+// The variant for steps that rarely reach the function phase (the host's
+// `scan` choice): per-warp scan-ahead (1), or CTA compaction (2) — bit-exact,
+// but on c1 6.4e9 vs 9.56e9 trajectory-steps/s: while the packed function
+// phases run, most warps of the CTA wait at the barrier and the few working
+// ones cannot hide the phase's load latency.
+#ifndef PBN_LANE_COMPACT
+#define PBN_LANE_COMPACT 0
+#endif
+constexpr int kRareFnMode = PBN_LANE_COMPACT ? 2 : 1;
+const char* lane_rare_fn_name() { return kRareFnMode == 2 ? "compact" : "scan"; }
+// Shared memory of the CTA-compaction variant: warp counts + the task list.
+std::size_t lane_cta_bytes() { return kRareFnMode == 2 ? 4 * 32 + 2 * 32 * kLaneMaxWarps + 16 : 0; }
 
 // The lane kernel serves lanes_per_traj = 1 for networks up to 255 kept nodes
 // (8 state words; larger ones use ensemble.cu's one-lane sub-warps).
@@ -506,8 +584,8 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
                                  std::uint32_t* launches) {
   const lane_kernel_fn fn =
       stream_kind == STREAM_U53
-          ? (scan ? pick_lane_place<STREAM_U53, true>(place) : pick_lane_place<STREAM_U53, false>(place))
-          : (scan ? pick_lane_place<STREAM_U32, true>(place) : pick_lane_place<STREAM_U32, false>(place));
+          ? (scan ? pick_lane_place<STREAM_U53, kRareFnMode>(place) : pick_lane_place<STREAM_U53, 0>(place))
+          : (scan ? pick_lane_place<STREAM_U32, kRareFnMode>(place) : pick_lane_place<STREAM_U32, 0>(place));
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t grid = (rp.n_traj + threads - 1) / threads;
   const std::size_t staged = stream_kind == STREAM_U53 ? staged_prefix<STREAM_U53>(h, place)
@@ -515,7 +593,7 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
   const std::size_t smem = staged +
                            static_cast<std::size_t>(warps_per_cta) *
                                lane_warp_words(h, rp.node_counts != nullptr) * 4 +
-                           16;
+                           (scan ? lane_cta_bytes() : 0) + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
