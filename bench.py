@@ -61,6 +61,7 @@ def workload_text(name, p=None):
 PHILOX_BLOCKS_PER_S = 4.797e11
 
 METRIC = "node-updates/sec"
+BACKEND = os.environ.get("PBN_BENCH_BACKEND", "nccl")
 UNIT = "node-updates/s"
 
 
@@ -429,11 +430,20 @@ def run_ours(a):
     if world > 1:
         import torch.distributed as dist
 
+        # PBN_BENCH_BACKEND=gloo (tests only): host-side collectives over gloo and
+        # every rank on the visible devices round-robin — exercises the N > 1
+        # code path on a one-GPU box (the device group then falls back)
+        if BACKEND != "nccl":
+            local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    rdev = dev if BACKEND == "nccl" else torch.device("cpu")  # collective tensors
     if a.mode == "estimate" or (a.mode == "auto" and WORKLOADS[a.config]["n_steps"] == 0):
         run_estimate_mode(a, torch, dist if world > 1 else None, rank, world, local, dev)
         if world > 1:
@@ -490,14 +500,14 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
     my_ms = sum(ev_ms)
-    t_ms = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    t_ms = torch.tensor([my_ms], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)  # measurement: max over ranks
     total_ms = float(t_ms.item())
     # the single collective of the path: one all-reduce of the pooled counts
     mine = pooled(counts.cpu().numpy().view(np.uint64))
     mine[6] = fn_steps  # function-phase steps over all timed launches
-    totals = allreduce_totals(mine, device=dev)
+    totals = allreduce_totals(mine, device=rdev)
     fn_total = int(totals[6])
     traj_steps = n_traj * world * sim_steps * a.steps
     value = traj_steps * flat.n_kept / (total_ms / 1e3)
@@ -514,20 +524,33 @@ def run_ours(a):
                                      C.cast(host_states.data_ptr(), C.POINTER(C.c_uint64)),
                                      C.cast(host_counts.data_ptr(), C.POINTER(C.c_uint64)), None))
 
-    grp = None
+    grp, e2e_path = None, "pbn_gpu_run (C-ABI, host buffers)"
     if world > 1:
         # N > 1: end to end through the C-ABI device group (pbn_group_run):
         # host rows in, this rank's launch, pooling kernels, ONE ncclAllReduce
-        # of the pooled counts, host rows + job totals out
-        ids = [pb.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(ids, src=0)
-        grp = pb.GpuGroup(plan, device=local, nranks=world, rank=rank, nccl_id=ids[0])
-        g_states = np.zeros((n_traj, words), np.uint64)
+        # of the pooled counts, host rows + job totals out. If the group cannot
+        # be built on every rank, every rank falls back to pbn_gpu_run (the
+        # reason goes into the line) rather than failing the run.
+        ok, why = 1, ""
+        try:
+            ids = [pb.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            grp = pb.GpuGroup(plan, device=local, nranks=world, rank=rank, nccl_id=ids[0])
+        except Exception as e:  # noqa: BLE001
+            ok, why = 0, f"{type(e).__name__}: {e}"
+        flag = torch.tensor([ok], dtype=torch.int32, device=rdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            e2e_path = ("pbn_group_run (C-ABI device group: one ncclAllReduce of the pooled "
+                        "counts)")
+            g_states = np.zeros((n_traj, words), np.uint64)
 
-        def e2e_one(n_steps, s0):  # noqa: F811
-            nonlocal g_states
-            g_states, _, _, _ = grp.simulate(42, n_traj * world, n_steps, step_begin=s0,
-                                             states=g_states, pred=pred, stream=stream)
+            def e2e_one(n_steps, s0):  # noqa: F811
+                nonlocal g_states
+                g_states, _, _, _ = grp.simulate(42, n_traj * world, n_steps, step_begin=s0,
+                                                 states=g_states, pred=pred, stream=stream)
+        else:
+            e2e_path += f" (device group unavailable: {why or 'on another rank'})"
 
     e2e_one(max(1, sim_steps // 10), 0)
     if world > 1:
@@ -536,7 +559,7 @@ def run_ours(a):
     for k in range(a.steps):
         e2e_one(sim_steps, k * sim_steps)
     e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_val = traj_steps * flat.n_kept / float(e2e_t.item())
@@ -616,8 +639,7 @@ def run_ours(a):
         "node_updates_per_s_original_n": traj_steps * w.n / (total_ms / 1e3),
         "fn_phase_fraction": fn_total / traj_steps,
         "e2e": {"value": e2e_val, "unit": UNIT,
-                "path": ("pbn_group_run (C-ABI device group: one ncclAllReduce of the pooled "
-                         "counts)" if world > 1 else "pbn_gpu_run (C-ABI, host buffers)"),
+                "path": e2e_path,
                 "h2d_bytes_per_step": n_traj * words * 8,
                 "d2h_bytes_per_step": n_traj * words * 8 + n_traj * 8 * 8},
         "gpu_launches": launches,
