@@ -25,7 +25,7 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             int stream_kind, std::uint32_t lpt, std::uint32_t warps_per_cta,
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
-                            std::uint32_t* launches);
+                            std::uint32_t* launches, bool pert_dom);
 cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
                                  int stream_kind, bool scan, std::uint32_t warps_per_cta,
                                  const dev_run_params& rp, std::uint64_t* d_states,
@@ -64,6 +64,7 @@ struct pbn_gpu {
   int device = 0;
   encoded_plan ep;
   int place = 0;  // PLACE_* of ensemble.cu
+  bool place_fixed = false;  // set by pbn_gpu_set_placement (not "auto")
   std::uint32_t smem_optin = 0, sms = 0;
   std::uint8_t* d_blob = nullptr;
   // scratch for the host-buffer entry point
@@ -127,6 +128,12 @@ constexpr std::uint32_t kStateReserve = 24 * 1024;  // smem kept for trajectory 
 // Lane kernel: scan phase A ahead per lane when fewer steps than this reach
 // the function phase (c1: 0.37 -> +22%; c3: 0.91 -> -17%).
 constexpr double kScanBelow = 0.65;
+// Sub-warp kernel, perturbation-dominated launches: when fewer steps than this
+// reach the function phase (c5 at p >= 0.01: < 1e-8), the launch stages
+// nothing (every shared-memory byte the plan does not take stays L1 for the
+// 256 KiB perturbation-cell words), runs 32 warps per CTA and prefetches the
+// next step's phase A (ensemble.cu PF): c5 p = 0.1 1.71e9 -> see DESIGN §7a.
+constexpr double kPertDominated = 0.02;
 
 // Probability that a step reaches the function phase: no kept node flips
 // (every pattern draw returns 0, or every Bernoulli draw misses) and the leaf
@@ -196,7 +203,8 @@ int next_lower_place(int place) {
 // Warps per CTA: enough resident slots for the whole ensemble in one wave
 // (grid ~ #SMs), bounded by 32 warps and by the shared memory left for states.
 std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t lpt,
-                         bool node_counts, std::uint32_t min_staged = 0) {
+                         bool node_counts, std::uint32_t min_staged = 0,
+                         std::uint32_t max_warps_lpt32 = 28) {
   if (lpt == 1 && lane_kernel_fits(g.ep.h)) {  // lane kernel: 32 trajectories per warp
     const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) + 31) / 32;
     std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
@@ -209,7 +217,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
   }
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
-  w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? 28 : 32, w));
+  w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? max_warps_lpt32 : 32, w));
   const std::uint64_t stride =
       (2 * g.ep.h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
@@ -279,6 +287,7 @@ struct launch_choice {
   int place = 0;
   bool lane = false, scan = false;
   int gm = 0;
+  bool pert_dom = false;  // sub-warp PF kernel (kPertDominated)
 };
 
 launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, std::uint32_t stream) {
@@ -290,9 +299,18 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, st
   // GM 4 kernels stage the compact single-node group records at any placement
   const std::uint32_t min_staged = c.gm == 4 ? g.ep.h.off_sfn : 0u;
   const int place0 = g.place;
+  // perturbation-dominated launch of a k = 16 plan with one phase-A block per
+  // lane, placement left to the engine: global placement, PF kernel
+  const std::uint32_t nb0 = (g.ep.h.g + g.ep.h.has_leaf + 3) / 4;
+  c.pert_dom = !c.lane && c.lpt == 32 && !g.place_fixed && g.p_fn < kPertDominated &&
+               g.ep.h.pert_mode == 0 && g.ep.h.k == 16 && nb0 <= 32;
+  if (c.pert_dom) {
+    g.place = 0;
+    c.gm = 0;
+  }
   for (;;) {
     try {
-      c.warps = pick_warps(g, n_traj, c.lpt, nc, min_staged);
+      c.warps = pick_warps(g, n_traj, c.lpt, nc, c.pert_dom ? 0u : min_staged, c.pert_dom ? 32u : 28u);
       break;
     } catch (const resource_error&) {
       if (g.place == 0) {
@@ -314,7 +332,9 @@ std::string kernel_name(const launch_choice& c, std::uint32_t stream) {
   std::string s = c.lane ? std::string("lane<") + (c.scan ? lane_rare_fn_name() : "lockstep")
                          : "subwarp<lpt=" + std::to_string(c.lpt) + ",gather=" + gms[c.gm];
   s += std::string(",stream=") + (stream == PBN_STREAM_U53 ? "u53" : "u32");
-  s += std::string(",place=") + places[c.place] + ",warps=" + std::to_string(c.warps) + ">";
+  s += std::string(",place=") + places[c.place] + ",warps=" + std::to_string(c.warps);
+  if (c.pert_dom) s += ",pa_prefetch";
+  s += ">";
   return s;
 }
 
@@ -337,7 +357,7 @@ void run_device(pbn_gpu& g, const pbn_run_args& a, std::uint64_t* d_states,
       c.lane ? launch_lane_ensemble(g.ep.h, g.d_blob, c.place, static_cast<int>(a.stream), c.scan,
                                     c.warps, rp, d_states, d_counts, stream, &g.launches)
              : launch_ensemble(g.ep.h, g.d_blob, c.place, static_cast<int>(a.stream), c.lpt,
-                               c.warps, rp, d_states, d_counts, stream, &g.launches);
+                               c.warps, rp, d_states, d_counts, stream, &g.launches, c.pert_dom);
   ck(e, "ensemble launch");
 }
 
@@ -616,6 +636,7 @@ int pbn_gpu_set_placement(pbn_gpu* g, uint32_t placement) {
     if (need_bytes + 4096 > g->smem_optin)
       throw resource_error("requested placement does not fit in shared memory");
     g->place = want;
+    g->place_fixed = true;
   });
 }
 

@@ -18,6 +18,11 @@
 //                      where T = ceil(cut * 2^(53-k)); cells whose cut rounds to
 //                      the whole range store (T=0, alias=c).
 //   pert32[2^k]   u32  the same for the U32 stream with 32-k threshold bits.
+//   pert53h[2^k]  u32  the high words of pert53 (cell result + the threshold's top
+//                      32-k bits), never staged: launches that read the cells
+//                      through L1/L2 decide on these (half the cache footprint of
+//                      the 8-byte cells: 256 KiB at k = 16) and touch pert53
+//                      itself only on a tie.
 //   groups[G]     uint4 {offset, fn_begin, alias_begin, alias_size | (members-1)<<24};
 //                      the A alias groups come first (grouping.hpp: multi-function
 //                      groups precede single-function ones), so the function phase
@@ -136,6 +141,8 @@ struct dev_plan_header {
   std::uint32_t has_leaf;        // phase A ends with the leaf draw
   std::uint64_t pthr53;          // Bernoulli: flip iff R < ceil(p * 2^53) << 11 (raw word)
   std::uint64_t pthr32;          //            flip iff r32 < ceil(p * 2^32)
+  std::uint32_t off_pert53h;     // high words of pert53 (unstaged tail)
+  std::uint32_t reserved1;
 };
 
 // Compiled predicate: the state satisfies it iff for every i,

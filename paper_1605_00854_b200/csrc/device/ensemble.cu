@@ -42,6 +42,20 @@ constexpr bool kUseRg2 = PBN_RG2 != 0;
 #define PBN_PLAIN_SHFL 1
 #endif
 constexpr bool kPlainShfl = PBN_PLAIN_SHFL != 0;
+// Phase-A prefetch (the PF kernels: perturbation-dominated launches of k = 16
+// plans with at most one phase-A block per lane): the class of a step is a
+// function of the stream alone, so the next step's phase-A Philox block and its
+// four perturbation-cell words are fetched into registers while the current
+// step finishes (1: issued before the step's ballots; 2: after the function
+// phase). Measured on every kernel (A/B on one box): c5 p >= 0.01 +6 %, but
+// c2 -10 % and c5 p <= 1e-3 -3..5 % (the hot function-phase loops lose
+// registers), so only launches that almost never reach the function phase
+// take it (capi.cpp kPertDominated).
+#ifndef PBN_PA_PREFETCH
+#define PBN_PA_PREFETCH 1
+#endif
+constexpr int kPaPrefetch = PBN_PA_PREFETCH;
+constexpr int kMaxWarpsPf = 32;  // PF kernels: 64 registers, 32 warps per CTA
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
@@ -51,8 +65,8 @@ constexpr int kMaxWarpsLpt32 = 28;
 // lane with shuffles (RG), 2 RG with the compact single-node records (SC), 3
 // two state words per lane (RG2, n' <= 2047) for the single-node groups
 // (general groups gather from shared memory: they run under divergence).
-template <int LPT, int STREAM, int PLACE, int GM>
-__global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
+template <int LPT, int STREAM, int PLACE, int GM, bool PF = false>
+__global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024, 1)
     pbn_ensemble_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                         const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
                         std::uint64_t* __restrict__ counts) {
@@ -76,8 +90,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
   const std::uint8_t* pcells = pert_cells<STREAM, PLACE>(smem, gblob, h);
-  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pcells);
-  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pcells);
+  const std::uint8_t* pfast = pert_fast_base<STREAM, GP>(pcells, gblob, h);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
@@ -532,6 +545,24 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
   const uint4 pam0 = make_uint4(pa_mask(r, 0), pa_mask(r, 1), pa_mask(r, 2), pa_mask(r, 3));
   const std::uint32_t lfe0 = lf_elem(r);
 
+  // Phase-A prefetch (kPaPrefetch): lane r < nb0 fetches step s's block r and
+  // the high words (U32: the words) of its four perturbation cells.
+  const bool pa_pf = PF && kPaPrefetch != 0 && h.pert_mode == 0 && k == 16 && nb0 <= LPT;
+  uint4 pfx = make_uint4(0, 0, 0, 0), pfe = make_uint4(0, 0, 0, 0);
+  auto pa_fetch = [&](std::uint64_t s) {
+    const step_philox spn = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+    pfx = philox_block(spn, r, rp.rk0, rp.rk1);
+    auto cell = [&](std::uint32_t hw) -> std::uint32_t {
+      if constexpr (STREAM == STREAM_U53)
+        return pert53_hi_word<GP>(pfast, hw >> 16);
+      else
+        return ldp<GP>(reinterpret_cast<const std::uint32_t*>(pfast) + (hw >> 16));
+    };
+    pfe = make_uint4(cell(pfx.x), cell(pfx.y), cell(pfx.z), cell(pfx.w));
+  };
+  if constexpr (PF)
+    if (pa_pf && r < nb0) pa_fetch(rp.step_begin);
+
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
   std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
@@ -589,7 +620,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       bool rare = false, lf = false;
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e)
-        c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), false, 0u, rare);
+        c[e] = pa_draw<STREAM, GP, BERN>(h, gblob, pfast, k, pick32(x, e), false, 0u, rare);
       if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
       if constexpr (STREAM == STREAM_U53) {
         if (__builtin_expect(rare, 0)) {
@@ -597,7 +628,7 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
           bool unused = false;
 #pragma unroll
           for (std::uint32_t e = 0; e < DPB; ++e)
-            c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), true, pick32(y, e), unused);
+            c[e] = pa_draw<STREAM, GP, BERN>(h, gblob, pfast, k, pick32(x, e), true, pick32(y, e), unused);
           if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), true, pick32(y, lfe), unused);
         }
       }
@@ -635,6 +666,44 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
         }
       }
     };
+    // The same block from the prefetched words (k = 16, block r): pattern
+    // c = draw's top 16 bits unless its next 16 bits reach the cell's
+    // threshold bits (then the cell's alias), kernel_common.cuh pert_draw53_hi
+    // / pert_draw32; a U53 tie on those bits redoes the block exactly.
+    auto phase_a_prefetched = [&]() {
+      const uint4 x = pfx, ce = pfe;
+      std::uint32_t c[DPB];
+      bool rare = false, lf = false;
+#pragma unroll
+      for (std::uint32_t e = 0; e < DPB; ++e) {
+        const std::uint32_t hw = pick32(x, e), cw = pick32(ce, e);
+        const std::uint32_t a = hw & 0xFFFFu, b = cw & 0xFFFFu;
+        if constexpr (STREAM == STREAM_U53) rare = rare || a == b;
+        c[e] = a < b ? (hw >> 16) : (cw >> 16);
+      }
+      if (lfe0 < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe0), false, 0u, rare);
+      if constexpr (STREAM == STREAM_U53) {
+        if (__builtin_expect(rare, 0)) {
+          const uint4 y = philox_lo_block(sp, r, rp.rk0, rp.rk1);
+          bool unused = false;
+#pragma unroll
+          for (std::uint32_t e = 0; e < DPB; ++e)
+            c[e] = pa_draw<STREAM, GP, false>(h, gblob, pfast, k, pick32(x, e), true, pick32(y, e), unused);
+          if (lfe0 < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe0), true, pick32(y, lfe0), unused);
+        }
+      }
+      leaf = leaf || lf;
+      const std::uint32_t w0 = (c[0] & pam0.x) | ((c[1] & pam0.y) << 16);
+      const std::uint32_t w1 = (c[2] & pam0.z) | ((c[3] & pam0.w) << 16);
+      if (__builtin_expect((w0 | w1) != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
+        flip = true;
+        uint2* w = reinterpret_cast<uint2*>(Sc) + r;
+        uint2 v = *w;
+        v.x ^= w0;
+        v.y ^= w1;
+        *w = v;
+      }
+    };
     auto phase_a = [&](auto bern_c, auto wpb_c) {
       if (nb0 <= LPT) {  // launch-uniform: at most one block per lane (masks precomputed)
         if (r < nb0) phase_a_block(r, pam0, lfe0, bern_c, wpb_c);
@@ -644,7 +713,12 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
                         lf_elem(b), bern_c, wpb_c);
       }
     };
-    if (h.pert_mode != 0)  // plan-uniform
+    if (PF && pa_pf) {  // launch-uniform
+      if (r < nb0) {
+        phase_a_prefetched();
+        if constexpr (kPaPrefetch == 1) pa_fetch(s + 1);
+      }
+    } else if (h.pert_mode != 0)  // plan-uniform
       phase_a(std::true_type{}, std::integral_constant<std::uint32_t, 0>{});
     else if (k == 16)
       phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 2>{});
@@ -810,6 +884,9 @@ __global__ void __launch_bounds__(LPT == 32 ? kMaxWarpsLpt32 * 32 : 1024, 1)
       else
         ++nfn;
     }
+
+    if constexpr (PF && kPaPrefetch == 2)
+      if (pa_pf && r < nb0) pa_fetch(s + 1);
 
     // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
     const std::uint32_t hit = pred_eval(cur ? S1 : S0);
@@ -1012,9 +1089,19 @@ kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
   }
 }
 
-kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm) {
+kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm, bool pert_dom) {
+#ifdef PBN_FAST_BUILD  // register-allocation experiments: the headline instantiations only
+  if (pert_dom) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 0, true>;
+  if (gm == 4) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 4>;
+  if (gm == 0) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_CORE, 0>;
+  return pbn_ensemble_kernel<32, STREAM_U53, PLACE_TABLES, 2>;
+#else
+  if (pert_dom)  // perturbation-dominated launch: plan through L1/L2, phase-A prefetch
+    return stream == STREAM_U53 ? pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 0, true>
+                                : pbn_ensemble_kernel<32, STREAM_U32, PLACE_GLOBAL, 0, true>;
   return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, gm)
                               : pick_lpt<STREAM_U32>(lpt, place, gm);
+#endif
 }
 
 std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
@@ -1041,9 +1128,9 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                             int stream_kind, std::uint32_t lpt, std::uint32_t warps_per_cta,
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
-                            std::uint32_t* launches) {
-  const int gm = ensemble_gather_mode(h, lpt, stream_kind);
-  const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm);
+                            std::uint32_t* launches, bool pert_dom) {
+  const int gm = pert_dom ? 0 : ensemble_gather_mode(h, lpt, stream_kind);
+  const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm, pert_dom);
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;

@@ -180,17 +180,53 @@ __device__ __forceinline__ std::uint32_t pick32(const uint4& x, std::uint32_t e)
   return (e & 2u) ? hi : lo;
 }
 
+#ifndef PBN_PERT53H
+#define PBN_PERT53H 1
+#endif
+constexpr bool kPert53h = PBN_PERT53H != 0;  // 0: A/B switch, always the 8-byte cells
+
+// The launch's perturbation cells as the fast paths read them: U53 launches
+// that read the cells through L1/L2 (G) use the dense high-word array
+// pert53h; otherwise the stream's (staged or global) cells.
+template <int STREAM, bool G>
+__device__ __forceinline__ const std::uint8_t* pert_fast_base(const std::uint8_t* pcells,
+                                                              const std::uint8_t* gblob,
+                                                              const dev_plan_header& h) {
+  if constexpr (G && STREAM == 0 && kPert53h)
+    return gblob + h.off_pert53h;
+  else
+    return pcells;
+}
+// The high word of U53 cell c.
+template <bool G>
+__device__ __forceinline__ std::uint32_t pert53_hi_word(const std::uint8_t* pfast, std::uint32_t c) {
+  if constexpr (G && kPert53h)
+    return __ldg(reinterpret_cast<const std::uint32_t*>(pfast) + c);
+  else
+    return ldp<G>(reinterpret_cast<const std::uint32_t*>(pfast) + 2 * c + 1);
+}
+// The full 8-byte U53 cells (the exact paths): not kept in a register by G
+// launches (the header and the blob pointer are kernel parameters).
+template <bool G>
+__device__ __forceinline__ const std::uint64_t* pert53_cells(const std::uint8_t* pfast,
+                                                             const std::uint8_t* gblob,
+                                                             const dev_plan_header& h) {
+  if constexpr (G && kPert53h)
+    return reinterpret_cast<const std::uint64_t*>(gblob + h.off_pert53);
+  else
+    return reinterpret_cast<const std::uint64_t*>(pfast);
+}
 // Perturbation cell lookup (alias.hpp:70-76 with N = 2^k), integer form on
 // the raw draw word R = hi << 32 | lo: the cell index is the top k bits, the
 // threshold compare runs on the remaining 64-k bits (dev_plan.h pert53).
 // Fast form on the high word alone: decided unless its 32-k compare bits tie
 // with the cell's (`rare`; pert_draw53_exact then needs the low word).
 template <bool G>
-__device__ __forceinline__ std::uint32_t pert_draw53_hi(const std::uint64_t* cells, std::uint32_t hi,
+__device__ __forceinline__ std::uint32_t pert_draw53_hi(const std::uint8_t* pfast, std::uint32_t hi,
                                                         std::uint32_t k, bool& rare) {
   const std::uint32_t c = hi >> (32 - k);
   const std::uint32_t hmask = 0xFFFFFFFFu >> k;
-  const std::uint32_t ehi = ldp<G>(reinterpret_cast<const std::uint32_t*>(cells + c) + 1);
+  const std::uint32_t ehi = pert53_hi_word<G>(pfast, c);
   const std::uint32_t a = hi & hmask, b = ehi & hmask;
   rare = rare || a == b;
   return a < b ? c : (ehi >> (32 - k));
@@ -213,8 +249,8 @@ __device__ __forceinline__ std::uint32_t pert_draw53_exact(const std::uint64_t* 
 // never rare.
 template <int STREAM, bool G, bool BERN>
 __device__ __forceinline__ std::uint32_t pa_draw(const dev_plan_header& h,
-                                                 const std::uint64_t* pert53,
-                                                 const std::uint32_t* pert32, std::uint32_t k,
+                                                 const std::uint8_t* gblob,
+                                                 const std::uint8_t* pfast, std::uint32_t k,
                                                  std::uint32_t hw, bool exact, std::uint32_t lo,
                                                  bool& rare);
 // The leaf draw (engine.hpp:268, reduction.hpp:98): u > t.
@@ -242,8 +278,8 @@ __device__ __forceinline__ std::uint32_t pert_draw32(const std::uint32_t* cells,
 
 template <int STREAM, bool G, bool BERN>
 __device__ __forceinline__ std::uint32_t pa_draw(const dev_plan_header& h,
-                                                 const std::uint64_t* pert53,
-                                                 const std::uint32_t* pert32, std::uint32_t k,
+                                                 const std::uint8_t* gblob,
+                                                 const std::uint8_t* pfast, std::uint32_t k,
                                                  std::uint32_t hw, bool exact, std::uint32_t lo,
                                                  bool& rare) {
   if constexpr (BERN) {
@@ -256,10 +292,10 @@ __device__ __forceinline__ std::uint32_t pa_draw(const dev_plan_header& h,
       return hw < h.pthr32 ? 1u : 0u;
     }
   } else if constexpr (STREAM == STREAM_U53) {
-    if (exact) return pert_draw53_exact(pert53, raw53{hw, lo}, k);
-    return pert_draw53_hi<G>(pert53, hw, k, rare);
+    if (exact) return pert_draw53_exact(pert53_cells<G>(pfast, gblob, h), raw53{hw, lo}, k);
+    return pert_draw53_hi<G>(pfast, hw, k, rare);
   } else {
-    return pert_draw32<G>(pert32, hw, k);
+    return pert_draw32<G>(reinterpret_cast<const std::uint32_t*>(pfast), hw, k);
   }
 }
 

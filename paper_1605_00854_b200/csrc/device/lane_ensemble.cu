@@ -73,8 +73,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   const std::uint8_t* core = GC ? gblob : smem;
   const std::uint8_t* tab = GT ? gblob + h.off_tables : smem + h.off_tables;
   const std::uint8_t* pcells = pert_cells<STREAM, PLACE>(smem, gblob, h);
-  const std::uint64_t* pert53 = reinterpret_cast<const std::uint64_t*>(pcells);
-  const std::uint32_t* pert32 = reinterpret_cast<const std::uint32_t*>(pcells);
+  const std::uint8_t* pfast = pert_fast_base<STREAM, GP>(pcells, gblob, h);
   const uint4* groups = reinterpret_cast<const uint4*>(core + h.off_groups);
   const uint4* fns = reinterpret_cast<const uint4*>(core + h.off_fns);
   const uint2* grec = reinterpret_cast<const uint2*>(core + h.off_grec);
@@ -262,7 +261,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
       bool rare = false, lf = false;
 #pragma unroll
       for (std::uint32_t e = 0; e < DPB; ++e)
-        c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), false, 0u, rare);
+        c[e] = pa_draw<STREAM, GP, BERN>(h, gblob, pfast, k, pick32(x, e), false, 0u, rare);
       if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
       if constexpr (STREAM == STREAM_U53) {
         if (__builtin_expect(rare, 0)) {
@@ -270,7 +269,7 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
           bool unused = false;
 #pragma unroll
           for (std::uint32_t e = 0; e < DPB; ++e)
-            c[e] = pa_draw<STREAM, GP, BERN>(h, pert53, pert32, k, pick32(x, e), true, pick32(y, e), unused);
+            c[e] = pa_draw<STREAM, GP, BERN>(h, gblob, pfast, k, pick32(x, e), true, pick32(y, e), unused);
           if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), true, pick32(y, lfe), unused);
         }
       }

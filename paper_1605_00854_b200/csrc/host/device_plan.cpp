@@ -485,6 +485,9 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   // FP64 cut-offs for the rare exact path: read through L1/L2, never staged
   h.off_acut = section(8 * acut.size());
   h.off_aidx = section(4 * aidx.size());
+  std::vector<std::uint32_t> pert53h(pert53.size());
+  for (std::size_t c = 0; c < pert53.size(); ++c) pert53h[c] = static_cast<std::uint32_t>(pert53[c] >> 32);
+  h.off_pert53h = section(4 * pert53h.size());
   if (h.fn_base || h.cell_base) {
     h.off_fns_s = section(4 * fns_s.size());
     h.off_acell_s = section(4 * acell_s.size());
@@ -499,6 +502,7 @@ encoded_plan encode_plan(const pbn_plan_view& v) {
   put(ep.blob, h.off_sfn, sfn);
   put(ep.blob, h.off_pert53, pert53);
   put(ep.blob, h.off_pert32, pert32);
+  put(ep.blob, h.off_pert53h, pert53h);
   put(ep.blob, h.off_groups, groups);
   put(ep.blob, h.off_fns, fns);
   put(ep.blob, h.off_grec, grec);

@@ -16,8 +16,8 @@ for line in log.splitlines():
     if cur is None:
         continue
     m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
-    if m:
-        cur["spill"] = int(m.group(1)) + int(m.group(2))
+    if m:  # the entry's own line and its out-of-line device functions': keep the sum
+        cur["spill"] = cur.get("spill", 0) + int(m.group(1)) + int(m.group(2))
     m = re.search(r"Used (\d+) registers", line)
     if m:
         cur["regs"] = int(m.group(1))
