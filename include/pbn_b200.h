@@ -234,6 +234,24 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states_inout, uint6
 /* Device-resident: DEVICE pointers, asynchronous on `stream` (a cudaStream_t, 0 = legacy). */
 int pbn_gpu_run_device(pbn_gpu* g, const pbn_run_args* a, uint64_t* d_states,
                        uint64_t* d_counts, uint64_t* d_node_counts, void* stream);
+/* Forced-draw replay — the device counterpart of the reference tests'
+ * scripted_rng (tests/oracles.hpp:235-254; test_engine.cpp:89-153): trajectory
+ * t consumes draws[t * n_draws + (i mod n_draws)], i = 0, 1, ..., in exactly
+ * the reference's call order (engine.hpp:259-290: g perturbation draws; if no
+ * kept node flipped the leaf draw; if it did not fire one draw per
+ * multi-function group), for a->n_steps steps of a->n_traj trajectories
+ * (a->seed / stream ignored; step_begin 0, no flags, carried samples or
+ * series). The library lays the script out in the stream's (step, block)
+ * slots with the reference's own FP64 rules and the SAME sub-warp kernel
+ * source replays it (built with the draw blocks read from the script instead
+ * of Philox). Decisions run on r53 = floor(u * 2^53): a draw that is not a
+ * multiple of 2^-53 is accepted only if its rounding provably leaves the
+ * decision it feeds unchanged, else PBN_EUSAGE names it. consumed_out[t]
+ * (may be NULL) = draws trajectory t consumed (scripted_rng::consumed()).
+ * HOST buffers; counts_out may be NULL. Grouped plans (pert_mode 0) only. */
+int pbn_gpu_run_scripted(pbn_gpu* g, const pbn_run_args* a, const double* draws,
+                         uint64_t n_draws, uint64_t* states_inout, uint64_t* counts_out,
+                         uint64_t* consumed_out);
 /* Stream known-answer hook: n Philox4x32-10 blocks of (4 x u32 counters) under key
  * = seed, computed by the device's Philox (tests compare with the oracle's). */
 int pbn_philox_kat(const uint32_t* ctr, uint32_t n, uint64_t seed, uint32_t* out);

@@ -174,6 +174,8 @@ def _load():
         "pbn_gpu_run": (I, [P, C.POINTER(RunArgs), C.POINTER(U64), C.POINTER(U64),
                             C.POINTER(U64)]),
         "pbn_gpu_run_device": (I, [P, C.POINTER(RunArgs), P, P, P, P]),
+        "pbn_gpu_run_scripted": (I, [P, C.POINTER(RunArgs), C.POINTER(C.c_double), U64,
+                                     C.POINTER(U64), C.POINTER(U64), C.POINTER(U64)]),
         "pbn_gpu_last_launches": (U32, [P]),
         "pbn_gpu_last_kernel": (I, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
         "pbn_gpu_plan_launch": (I, [P, U32, U32, U32, C.c_char_p, C.c_size_t,
@@ -220,7 +222,7 @@ EXPORTED_SYMBOLS = (
     "pbn_model_free", "pbn_prepare", "pbn_prepare_nodewise",
     "pbn_plan_get_view", "pbn_plan_reduced", "pbn_plan_groups", "pbn_compile_predicate",
     "pbn_plan_free", "pbn_device_count", "pbn_gpu_create", "pbn_gpu_set_placement", "pbn_gpu_info", "pbn_gpu_run",
-    "pbn_gpu_run_device", "pbn_gpu_last_launches", "pbn_gpu_last_kernel", "pbn_gpu_plan_launch",
+    "pbn_gpu_run_device", "pbn_gpu_run_scripted", "pbn_gpu_last_launches", "pbn_gpu_last_kernel", "pbn_gpu_plan_launch",
     "pbn_gpu_destroy", "pbn_estimate",
     "pbn_estimate_with_backend", "pbn_series_stats_host", "pbn_inverse_normal_cdf",
     "pbn_series_stats_device", "pbn_group_create", "pbn_nccl_unique_id", "pbn_group_create_rank",
@@ -613,6 +615,26 @@ class GpuEnsemble:
                                       C.c_void_p(d_counts),
                                       C.c_void_p(d_node_counts) if d_node_counts else None,
                                       C.c_void_p(cuda_stream)))
+
+    def simulate_scripted(self, draws, n_steps, states=None, pred=None):
+        """Forced-draw replay (pbn_gpu_run_scripted; the reference tests'
+        scripted_rng, tests/oracles.hpp:235-254): draws is (n_traj, n_draws)
+        float64 — or one row for one trajectory — consumed in the reference's
+        call order, wrapping around. Returns (states, counts, consumed)."""
+        draws = np.ascontiguousarray(np.atleast_2d(np.asarray(draws, np.float64)))
+        n_traj = draws.shape[0]
+        if states is None:
+            states = np.zeros((n_traj, self.words), np.uint64)
+        states = np.ascontiguousarray(states, np.uint64).copy()
+        assert states.shape == (n_traj, self.words)
+        counts = np.zeros((n_traj, COUNT_FIELDS), np.uint64)
+        consumed = np.zeros(n_traj, np.uint64)
+        a = self._args(0, 0, n_traj, n_steps, 0, pred, STREAM_U53)
+        _check(lib.pbn_gpu_run_scripted(self._h, C.byref(a),
+                                        draws.ctypes.data_as(C.POINTER(C.c_double)),
+                                        draws.shape[1], _u64p(states), _u64p(counts),
+                                        _u64p(consumed)))
+        return states, counts, consumed
 
     @property
     def device(self) -> int:

@@ -31,6 +31,10 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
                                  const dev_run_params& rp, std::uint64_t* d_states,
                                  std::uint64_t* d_counts, cudaStream_t stream,
                                  std::uint32_t* launches);
+cudaError_t launch_ensemble_script(const dev_plan_header& h, const std::uint8_t* d_blob,
+                                   std::uint32_t warps_per_cta, const dev_run_params& rp,
+                                   std::uint64_t* d_states, std::uint64_t* d_counts,
+                                   cudaStream_t stream);
 bool lane_kernel_fits(const dev_plan_header& h);
 int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
@@ -87,6 +91,15 @@ struct pbn_gpu {
   ws_buf ws[9];
   double p_fn = 1.0;  // probability that a step reaches the function phase
   double p_group_flip = 0.0;  // probability that a full perturbation group flips
+  // host copy of the plan's decision tables (pbn_gpu_run_scripted lays a
+  // sequential script out in the stream's slots with the reference's own rules)
+  struct script_tables {
+    double t = 1.0;
+    std::uint32_t groups = 0, size = 0, has_leaf = 0, pert_mode = 0;
+    std::uint64_t mask = 0;
+    std::vector<double> pert_cut, alias_cut;
+    std::vector<std::uint32_t> pert_alias, alias_idx, a_begin, a_size;  // a_*: the alias groups, in order
+  } st;
 };
 
 namespace {
@@ -605,6 +618,29 @@ int pbn_gpu_create(const pbn_plan_view* view, int device, uint32_t lpt, pbn_gpu*
     g->ep = encode_plan(*view);
     g->p_fn = fn_phase_probability(*view);
     g->p_group_flip = group_flip_probability(*view);
+    {
+      auto& st = g->st;
+      const pbn_plan_view& v = *view;
+      st.t = v.t;
+      st.groups = v.pert_groups;
+      st.size = v.pert_size;
+      st.has_leaf = v.has_leaf;
+      st.pert_mode = v.pert_mode;
+      st.mask = v.pert_mask;
+      if (v.pert_mode == 0 && v.pert_size) {
+        st.pert_cut.assign(v.pert_cut, v.pert_cut + v.pert_size);
+        st.pert_alias.assign(v.pert_alias, v.pert_alias + v.pert_size);
+      }
+      if (v.n_alias) {
+        st.alias_cut.assign(v.alias_cut, v.alias_cut + v.n_alias);
+        st.alias_idx.assign(v.alias_idx, v.alias_idx + v.n_alias);
+      }
+      for (std::uint32_t gi = 0; gi < v.n_groups; ++gi)
+        if (v.grp_alias_size[gi]) {
+          st.a_begin.push_back(v.grp_alias_begin[gi]);
+          st.a_size.push_back(v.grp_alias_size[gi]);
+        }
+    }
     ck(cudaSetDevice(device), "cudaSetDevice");
     int optin = 0, sms = 0;
     ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
@@ -706,6 +742,125 @@ int pbn_gpu_run(pbn_gpu* g, const pbn_run_args* a, uint64_t* states, uint64_t* c
     ck(cudaMemcpy(counts, g->d_counts, 8 * PBN_COUNT_FIELDS * static_cast<std::size_t>(a->n_traj),
                   cudaMemcpyDeviceToHost),
        "D2H");
+  });
+}
+
+// alias_table::next(rng) on one uniform (alias.hpp:70-76; the group draw of
+// engine.hpp:284-290 is the same rule on the group's slice).
+static std::uint32_t alias_next(double u01, const double* cut, const std::uint32_t* alias,
+                                std::uint32_t n) {
+  const double u = u01 * static_cast<double>(n);
+  std::uint32_t i = static_cast<std::uint32_t>(u);
+  if (i >= n) i = n - 1;
+  return (u - static_cast<double>(i)) < cut[i] ? i : alias[i];
+}
+
+int pbn_gpu_run_scripted(pbn_gpu* g, const pbn_run_args* a, const double* draws, uint64_t n_draws,
+                         uint64_t* states, uint64_t* counts, uint64_t* consumed) {
+  return guard([&] {
+    need(g, "gpu");
+    need(a, "args");
+    need(draws, "draws");
+    need(states, "states");
+    const auto& st = g->st;
+    const dev_plan_header& h = g->ep.h;
+    if (st.pert_mode != 0) throw std::invalid_argument("scripted replay serves grouped plans (pert_mode 0)");
+    if (n_draws == 0) throw std::invalid_argument("empty script");
+    if (a->step_begin != 0 || a->flags != 0 || a->tprev || a->series || a->thin_mode != 0)
+      throw std::invalid_argument("scripted replay: step_begin 0, no flags, no carried samples or series");
+    if (a->n_traj == 0) return;
+    const std::uint32_t A = static_cast<std::uint32_t>(st.a_size.size());
+    const std::uint32_t nb0 = (st.groups + st.has_leaf + 3) / 4;
+    const std::uint64_t bps = nb0 + (A + 3) / 4;
+    const std::uint64_t blocks = static_cast<std::uint64_t>(a->n_traj) * a->n_steps * bps;
+    if (blocks > (1ull << 26)) throw resource_error("script too long (2^26 draw blocks at most)");
+    // slack: the kernel computes whole chunks of 32 blocks past a region's last draw
+    std::vector<std::uint32_t> hi(4 * (blocks + 64), 0u), lo(4 * (blocks + 64), 0u);
+    // Every decision is made on the device in integers on r53 = floor(u * 2^53);
+    // a script value that is not a multiple of 2^-53 is accepted only if the
+    // reference's FP64 rule decides the same for u and for r53 * 2^-53.
+    auto put = [&](std::uint64_t slot, double u, std::uint64_t& r53) {
+      if (!(u >= 0.0 && u < 1.0)) throw std::invalid_argument("script draws must lie in [0, 1)");
+      r53 = static_cast<std::uint64_t>(u * 9007199254740992.0);  // exact: a power-of-two scale
+      const std::uint64_t raw = r53 << 11;
+      hi[slot] = static_cast<std::uint32_t>(raw >> 32);
+      lo[slot] = static_cast<std::uint32_t>(raw);
+    };
+    auto inexact = [](std::uint64_t i) {
+      return std::invalid_argument("script draw " + std::to_string(i) +
+                                   " is not a multiple of 2^-53 and its rounding changes a decision");
+    };
+    for (std::uint32_t t = 0; t < a->n_traj; ++t) {
+      const double* row = draws + static_cast<std::size_t>(t) * n_draws;
+      std::uint64_t pos = 0;
+      auto next = [&]() { return row[pos++ % n_draws]; };
+      for (std::uint64_t s = 0; s < a->n_steps; ++s) {
+        const std::uint64_t base = 4 * ((static_cast<std::uint64_t>(t) * a->n_steps + s) * bps);
+        bool perturbed = false;
+        for (std::uint32_t i = 0; i < st.groups; ++i) {  // engine.hpp:259-266
+          const double u = next();
+          std::uint64_t r53;
+          put(base + i, u, r53);
+          std::uint64_t c = alias_next(u, st.pert_cut.data(), st.pert_alias.data(), st.size);
+          const double uq = static_cast<double>(r53) * 0x1p-53;
+          if (uq != u && alias_next(uq, st.pert_cut.data(), st.pert_alias.data(), st.size) != c)
+            throw inexact(pos - 1);
+          if (i + 1 == st.groups) c &= st.mask;
+          perturbed = perturbed || c != 0;
+        }
+        if (perturbed) continue;  // engine.hpp:267
+        if (st.has_leaf) {        // engine.hpp:268, reduction.hpp:98
+          const double u = next();
+          std::uint64_t r53;
+          put(base + st.groups, u, r53);
+          const double uq = static_cast<double>(r53) * 0x1p-53;
+          if ((uq > st.t) != (u > st.t)) throw inexact(pos - 1);
+          if (u > st.t) continue;
+        }
+        for (std::uint32_t j = 0; j < A; ++j) {  // engine.hpp:284-290
+          const double u = next();
+          std::uint64_t r53;
+          put(base + 4ull * nb0 + j, u, r53);
+          const double* cut = st.alias_cut.data() + st.a_begin[j];
+          const std::uint32_t* idx = st.alias_idx.data() + st.a_begin[j];
+          const double uq = static_cast<double>(r53) * 0x1p-53;
+          if (uq != u && alias_next(uq, cut, idx, st.a_size[j]) != alias_next(u, cut, idx, st.a_size[j]))
+            throw inexact(pos - 1);
+        }
+      }
+      if (consumed) consumed[t] = pos;
+    }
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    pbn_run_args ua = *a;
+    ua.stream = PBN_STREAM_U53;
+    dev_run_params rp = make_params(*g, ua);
+    const std::size_t words = pbn_state_words(h.n_kept);
+    const std::size_t blk_bytes = 16 * (blocks + 64);
+    std::uint64_t* d_states = ws_take<std::uint64_t>(*g, 0, words * a->n_traj);
+    std::uint64_t* d_counts = ws_take<std::uint64_t>(*g, 1, static_cast<std::size_t>(a->n_traj) * PBN_COUNT_FIELDS);
+    uint4* d_hi = ws_take<uint4>(*g, 3, blocks + 64);
+    uint4* d_lo = ws_take<uint4>(*g, 4, blocks + 64);
+    ck(cudaMemcpy(d_states, states, 8 * words * a->n_traj, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_hi, hi.data(), blk_bytes, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_lo, lo.data(), blk_bytes, cudaMemcpyHostToDevice), "H2D");
+    rp.script_hi = d_hi;
+    rp.script_lo = d_lo;
+    rp.script_bps = bps;
+    // one trajectory per warp; warps per CTA by the shared memory the states take
+    const std::size_t slot_bytes = 4 * ((2 * h.sw32 + 32 * 4 * kChunkBlocks + 3) & ~3u);
+    std::uint32_t warps = static_cast<std::uint32_t>(std::min<std::size_t>(8, (g->smem_optin - 64) / slot_bytes));
+    if (warps == 0) throw resource_error("trajectory state does not fit in shared memory");
+    g->launches = 0;
+    ck(launch_ensemble_script(h, g->d_blob, warps, rp, d_states, d_counts, nullptr), "scripted launch");
+    g->launches = 1;
+    g->last_lpt = 32;
+    g->last_warps = warps;
+    g->last_place = 0;
+    g->last_kernel = "subwarp_script<lpt=32,gather=smem,stream=u53,place=global,warps=" + std::to_string(warps) + ">";
+    ck(cudaMemcpy(states, d_states, 8 * words * a->n_traj, cudaMemcpyDeviceToHost), "D2H");
+    if (counts)
+      ck(cudaMemcpy(counts, d_counts, 8 * PBN_COUNT_FIELDS * static_cast<std::size_t>(a->n_traj),
+                    cudaMemcpyDeviceToHost), "D2H");
   });
 }
 

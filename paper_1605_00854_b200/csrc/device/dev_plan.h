@@ -179,6 +179,14 @@ struct dev_run_params {
   // optional per-node one-counts (engine.hpp:378-379): n_traj x n_kept u64,
   // accumulated (+=) over the call's steps
   std::uint64_t* node_counts;
+  // scripted replay (pbn_gpu_run_scripted): the draws' raw words in the
+  // stream's slot layout — trajectory t, step i, block b at
+  // [(t * n_steps + i) * script_bps + b]: high words in script_hi, low words in
+  // script_lo (draw e of block b = word e; r53 = (hi << 32 | lo) >> 11)
+  const void* script_hi;  // 16-byte blocks
+  const void* script_lo;
+  std::uint64_t script_bps;
+  std::uint64_t reserved2;  // keeps the parameters that follow 16-byte aligned
 };
 
 }  // namespace pbn_b200

@@ -42,6 +42,22 @@ constexpr bool kUseRg2 = PBN_RG2 != 0;
 #define PBN_PLAIN_SHFL 1
 #endif
 constexpr bool kPlainShfl = PBN_PLAIN_SHFL != 0;
+
+// Block b of the current step's stream (high words) and its low block. The
+// scripted-replay translation unit (ensemble_script.cu includes this file
+// with PBN_SCRIPT_TU) reads caller-supplied draws laid out in the stream's own
+// (step, block) slots instead of computing Philox — the reference's
+// forced-draw traces (tests/oracles.hpp:235-254) replayed by the same kernel.
+#ifdef PBN_SCRIPT_TU
+#define pbn_ensemble_kernel pbn_ensemble_script_kernel
+#define PBN_BLK(b) __ldg(static_cast<const uint4*>(rp.script_hi) + script_row + (b))
+#define PBN_BLK_LO(b) __ldg(static_cast<const uint4*>(rp.script_lo) + script_row + (b))
+#define PBN_BLK_LO_INLINE(b) __ldg(static_cast<const uint4*>(rp.script_lo) + script_row + (b))
+#else
+#define PBN_BLK(b) philox_block(sp, (b), rp.rk0, rp.rk1)
+#define PBN_BLK_LO(b) philox_lo_block(sp, (b), rp.rk0, rp.rk1)
+#define PBN_BLK_LO_INLINE(b) philox_block(sp, (b) | kLoBlock, rp.rk0, rp.rk1)
+#endif
 // Phase-A prefetch (the PF kernels: perturbation-dominated launches of k = 16
 // plans with at most one phase-A block per lane): the class of a step is a
 // function of the stream alone, so the next step's phase-A Philox block and its
@@ -190,6 +206,9 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
 
   // the step's Philox constants (the redo path recomputes draws from them)
   step_philox sp{};
+#ifdef PBN_SCRIPT_TU
+  std::uint64_t script_row = 0;  // first block of the current step's draws
+#endif
   // U53: a combined-function choice made on the draw's high word alone is
   // exact unless the draw sits on a cell boundary or ties the cut point
   // (about N+1 draws in 2^32, dev_plan.h acell) or the group/launch takes the
@@ -503,8 +522,8 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       std::uint64_t r53 = 0;
       if (gi < A) {  // draw gi of phase B (alias groups come first)
         const std::uint32_t b = nb0 + gi / DPB, e = gi % DPB;
-        const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
-        const uint4 y = philox_block(sp, b | kLoBlock, rp.rk0, rp.rk1);
+        const uint4 x = PBN_BLK(b);
+        const uint4 y = PBN_BLK_LO_INLINE(b);
         r53 = ((static_cast<std::uint64_t>(pick32(x, e)) << 32) | pick32(y, e)) >> 11;
       }
       uint4 F;
@@ -595,7 +614,11 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
 
   for (std::uint64_t s = rp.step_begin; s < s_end; ++s) {
     std::uint32_t* Sc = cur ? S1 : S0;
+#ifdef PBN_SCRIPT_TU
+    script_row = (tloc * rp.n_steps + (s - rp.step_begin)) * rp.script_bps;
+#else
     sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+#endif
 
     // ---- phase A: grouped perturbation + leaf draw (draws 0..g). Every draw
     // of a block is looked up; a per-draw mask keeps full patterns for draws
@@ -615,7 +638,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
                              auto bern_c, auto wpb_c) {
       constexpr bool BERN = decltype(bern_c)::value;  // Method_old / Method_reduction plans
       constexpr std::uint32_t WPB = decltype(wpb_c)::value;
-      const uint4 x = philox_block(sp, b, rp.rk0, rp.rk1);
+      const uint4 x = PBN_BLK(b);
       std::uint32_t c[DPB];
       bool rare = false, lf = false;
 #pragma unroll
@@ -624,7 +647,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
       if constexpr (STREAM == STREAM_U53) {
         if (__builtin_expect(rare, 0)) {
-          const uint4 y = philox_lo_block(sp, b, rp.rk0, rp.rk1);
+          const uint4 y = PBN_BLK_LO(b);
           bool unused = false;
 #pragma unroll
           for (std::uint32_t e = 0; e < DPB; ++e)
@@ -684,7 +707,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       if (lfe0 < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe0), false, 0u, rare);
       if constexpr (STREAM == STREAM_U53) {
         if (__builtin_expect(rare, 0)) {
-          const uint4 y = philox_lo_block(sp, r, rp.rk0, rp.rk1);
+          const uint4 y = PBN_BLK_LO(r);
           bool unused = false;
 #pragma unroll
           for (std::uint32_t e = 0; e < DPB; ++e)
@@ -756,7 +779,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       if constexpr (kPhiloxPipeline) {
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
-          xb[q] = philox_block(sp, nb0 + q * LPT + r, rp.rk0, rp.rk1);
+          xb[q] = PBN_BLK(nb0 + q * LPT + r);
       }
       std::uint32_t jstart = 0;
       if constexpr (SC && DPB * CB == 2 && !kPhiloxPipeline) {
@@ -764,7 +787,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
         // bookkeeping; the general loop below takes the remaining chunks
         const std::uint32_t jfull = A1 & ~(2u * LPT - 1u);
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 2 * LPT) {
-          const uint4 x = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
+          const uint4 x = PBN_BLK(nb0 + j0 / DPB + r);
           *reinterpret_cast<uint4*>(dbuf + 4 * r) = x;
           __syncwarp(smask);
           single_pair(Sc, Sn, wreg, j0, 0);
@@ -775,7 +798,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
         // U32 compact: chunks of one single-node quad
         const std::uint32_t jfull = A1 & ~(4u * LPT - 1u);
         for (std::uint32_t j0 = 0; j0 < jfull; j0 += 4 * LPT) {
-          *reinterpret_cast<uint4*>(dbuf + 4 * r) = philox_block(sp, nb0 + j0 / DPB + r, rp.rk0, rp.rk1);
+          *reinterpret_cast<uint4*>(dbuf + 4 * r) = PBN_BLK(nb0 + j0 / DPB + r);
           __syncwarp(smask);
           single_quad(Sc, Sn, wreg, j0, 0);
           __syncwarp(smask);
@@ -786,7 +809,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
         if constexpr (!kPhiloxPipeline) {
 #pragma unroll
           for (std::uint32_t q = 0; q < CB; ++q)
-            xb[q] = philox_block(sp, nb0 + j0 / DPB + q * LPT + r, rp.rk0, rp.rk1);
+            xb[q] = PBN_BLK(nb0 + j0 / DPB + q * LPT + r);
         }
 #pragma unroll
         for (std::uint32_t q = 0; q < CB; ++q)
@@ -796,7 +819,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
         if constexpr (kPhiloxPipeline) {  // next chunk's blocks (unused after the last)
 #pragma unroll
           for (std::uint32_t q = 0; q < CB; ++q)
-            xb[q] = philox_block(sp, nb0 + (j0 / DPB) + (CB + q) * LPT + r, rp.rk0, rp.rk1);
+            xb[q] = PBN_BLK(nb0 + (j0 / DPB) + (CB + q) * LPT + r);
         }
         // rounds are taken in pairs: both rounds' loads are issued before
         // either ballot/store, so the two dependency chains overlap
@@ -967,6 +990,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
   }
 }
 
+#ifndef PBN_SCRIPT_TU
 // Pooled statistics of stored predicate series (estimator pilot): per
 // trajectory row, triple counts n_ijk at period kappa (t = 2k, 3k, ...), thinned
 // pair counts (t = k, 2k, ...) and ones in [1, len); summed over trajectories.
@@ -1154,5 +1178,28 @@ cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_
   pbn_philox_kat_kernel<<<(n + 127) / 128, 128, 0, stream>>>(d_ctr, k0, k1, d_out, n);
   return cudaGetLastError();
 }
+
+#else  // PBN_SCRIPT_TU: the scripted-replay launcher (capi.cpp pbn_gpu_run_scripted)
+
+// One instantiation: one trajectory per warp, U53 decisions, the whole plan
+// read through L1/L2, shared-memory gathers.
+cudaError_t launch_ensemble_script(const dev_plan_header& h, const std::uint8_t* d_blob,
+                                   std::uint32_t warps_per_cta, const dev_run_params& rp,
+                                   std::uint64_t* d_states, std::uint64_t* d_counts,
+                                   cudaStream_t stream) {
+  auto fn = pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 0>;
+  const std::uint32_t threads = warps_per_cta * 32;
+  const std::uint32_t grid = (rp.n_traj + warps_per_cta - 1) / warps_per_cta;
+  const std::size_t slot = (2 * h.sw32 + 32 * 4 * kChunkBlocks + (rp.node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
+  const std::size_t smem = static_cast<std::size_t>(warps_per_cta) * slot * 4 + 16;
+  cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  if (grid == 0) return cudaSuccess;
+  fn<<<grid, threads, smem, stream>>>(h, d_blob, rp, d_states, d_counts);
+  return cudaGetLastError();
+}
+#endif  // PBN_SCRIPT_TU
 
 }  // namespace pbn_b200

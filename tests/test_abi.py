@@ -19,7 +19,7 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ["pbn_model_parse", "pbn_prepare", "pbn_plan_get_view", "pbn_gpu_create",
-                 "pbn_gpu_run", "pbn_gpu_run_device", "pbn_compile_predicate", "pbn_estimate",
+                 "pbn_gpu_run", "pbn_gpu_run_device", "pbn_gpu_run_scripted", "pbn_compile_predicate", "pbn_estimate",
                  "pbn_last_error"]:
         assert must in names
 
