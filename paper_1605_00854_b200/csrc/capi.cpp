@@ -36,6 +36,7 @@ cudaError_t launch_ensemble_script(const dev_plan_header& h, const std::uint8_t*
                                    std::uint64_t* d_states, std::uint64_t* d_counts,
                                    cudaStream_t stream);
 bool lane_kernel_fits(const dev_plan_header& h);
+std::uint32_t pf_max_warps();
 int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
 std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
@@ -315,7 +316,7 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, st
   // perturbation-dominated launch of a k = 16 plan with one phase-A block per
   // lane, placement left to the engine: global placement, PF kernel
   const std::uint32_t nb0 = (g.ep.h.g + g.ep.h.has_leaf + 3) / 4;
-  c.pert_dom = !c.lane && c.lpt == 32 && !g.place_fixed && g.p_fn < kPertDominated &&
+  c.pert_dom = !c.lane && !nc && c.lpt == 32 && !g.place_fixed && g.p_fn < kPertDominated &&
                g.ep.h.pert_mode == 0 && g.ep.h.k == 16 && nb0 <= 32;
   if (c.pert_dom) {
     g.place = 0;
@@ -323,7 +324,7 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, st
   }
   for (;;) {
     try {
-      c.warps = pick_warps(g, n_traj, c.lpt, nc, c.pert_dom ? 0u : min_staged, c.pert_dom ? 32u : 28u);
+      c.warps = pick_warps(g, n_traj, c.lpt, nc, c.pert_dom ? 0u : min_staged, c.pert_dom ? pf_max_warps() : 28u);
       break;
     } catch (const resource_error&) {
       if (g.place == 0) {

@@ -71,7 +71,13 @@ constexpr bool kPlainShfl = PBN_PLAIN_SHFL != 0;
 #define PBN_PA_PREFETCH 1
 #endif
 constexpr int kPaPrefetch = PBN_PA_PREFETCH;
-constexpr int kMaxWarpsPf = 32;  // PF kernels: 64 registers, 32 warps per CTA
+#ifndef PBN_CARVEOUT
+#define PBN_CARVEOUT 1
+#endif
+#ifndef PBN_PF_WARPS
+#define PBN_PF_WARPS 28
+#endif
+constexpr int kMaxWarpsPf = PBN_PF_WARPS;  // PF kernels: warps per CTA (32 -> 64 registers: spills in the step loop)
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
@@ -82,7 +88,7 @@ constexpr int kMaxWarpsLpt32 = 28;
 // two state words per lane (RG2, n' <= 2047) for the single-node groups
 // (general groups gather from shared memory: they run under divergence).
 template <int LPT, int STREAM, int PLACE, int GM, bool PF = false>
-__global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024, 1)
+__global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32) * 32 : 1024, 1)
     pbn_ensemble_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                         const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
                         std::uint64_t* __restrict__ counts) {
@@ -582,6 +588,34 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
   if constexpr (PF)
     if (pa_pf && r < nb0) pa_fetch(rp.step_begin);
 
+  // PF kernels keep the state in registers between function phases: lane r
+  // owns words 2r, 2r+1 — exactly its phase-A block's patterns at k = 16 — so
+  // a perturbed step touches no shared memory; the rare function phase writes
+  // them to S0, runs as usual into S1 and reads them back.
+  uint2 sreg = make_uint2(0, 0);
+  if constexpr (PF)
+    if (2 * r < sw32) sreg = reinterpret_cast<const uint2*>(S0)[r];
+  // predicate on the register state: the terms on a lane's two words merged
+  // into one (mask, want) pair per word, fixed for the launch
+  uint2 pmask = make_uint2(0, 0), pwant = make_uint2(0, 0);
+  if constexpr (PF) {
+    for (std::uint32_t i = 0; i < rp.pred.n; ++i) {
+      const std::uint32_t w = rp.pred.w[i];
+      if ((w >> 1) != r) continue;
+      if (w & 1u) {
+        pmask.y |= rp.pred.mask[i];
+        pwant.y |= rp.pred.want[i];
+      } else {
+        pmask.x |= rp.pred.mask[i];
+        pwant.x |= rp.pred.want[i];
+      }
+    }
+  }
+  auto pred_eval_reg = [&]() -> std::uint32_t {
+    const bool ok = (((sreg.x & pmask.x) ^ pwant.x) | ((sreg.y & pmask.y) ^ pwant.y)) == 0;
+    return rp.pred.n != 0 && __all_sync(smask, ok) ? 1u : 0u;
+  };
+
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
   std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
@@ -718,14 +752,9 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       leaf = leaf || lf;
       const std::uint32_t w0 = (c[0] & pam0.x) | ((c[1] & pam0.y) << 16);
       const std::uint32_t w1 = (c[2] & pam0.z) | ((c[3] & pam0.w) << 16);
-      if (__builtin_expect((w0 | w1) != 0, 0)) {  // xor_chunk (bitstate.hpp:50-58)
-        flip = true;
-        uint2* w = reinterpret_cast<uint2*>(Sc) + r;
-        uint2 v = *w;
-        v.x ^= w0;
-        v.y ^= w1;
-        *w = v;
-      }
+      flip = (w0 | w1) != 0;  // xor_chunk (bitstate.hpp:50-58) on the register state
+      sreg.x ^= w0;
+      sreg.y ^= w1;
     };
     auto phase_a = [&](auto bern_c, auto wpb_c) {
       if (nb0 <= LPT) {  // launch-uniform: at most one block per lane (masks precomputed)
@@ -754,12 +783,22 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
 
     std::uint32_t ev = 0;  // this step's events (LANE_COUNTERS bit layout)
     if (any_flip) {
-      __syncwarp(smask);
+      if constexpr (!PF) __syncwarp(smask);
       if constexpr (LANE_COUNTERS)
         ev = 1u << 6;
       else
         ++npert;
     } else if (!any_leaf) {
+      if constexpr (PF) {
+        // ---- function phase of a perturbation-dominated launch (fewer than
+        // kPertDominated of the steps): the generic exact evaluation — every
+        // draw rebuilt as 53 bits, FP64 choices, parents from shared memory —
+        // between a store and a reload of the register state
+        if (2 * r < sw32) reinterpret_cast<uint2*>(S0)[r] = sreg;
+        redo_fn_phase(S0, S1);  // zeroes S1 and synchronises before and after
+        if (2 * r < sw32) sreg = reinterpret_cast<const uint2*>(S1)[r];
+        __syncwarp(smask);
+      } else {
       // ---- function phase, in lockstep rounds of LPT groups
       std::uint32_t* Sn = cur ? S0 : S1;
       for (std::uint32_t w = r; w < sw32; w += LPT) Sn[w] = 0;
@@ -902,6 +941,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       if constexpr (STREAM == STREAM_U53)
         if (__builtin_expect(__any_sync(smask, rare_acc), 0)) redo_fn_phase(Sc, Sn);
       cur ^= 1;
+      }  // !PF
       if constexpr (LANE_COUNTERS)
         ev = 1u << 5;
       else
@@ -912,7 +952,7 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
       if (pa_pf && r < nb0) pa_fetch(s + 1);
 
     // ---- statistics (engine.hpp:375-381) + sampled predicate transitions
-    const std::uint32_t hit = pred_eval(cur ? S1 : S0);
+    const std::uint32_t hit = PF && pa_pf ? pred_eval_reg() : pred_eval(cur ? S1 : S0);
     if constexpr (LANE_COUNTERS) {
       ev |= hit;
       if (++kphase == rp.kappa) {
@@ -964,7 +1004,11 @@ __global__ void __launch_bounds__(LPT == 32 && !PF ? kMaxWarpsLpt32 * 32 : 1024,
   {
     const std::uint32_t* Sf = cur ? S1 : S0;
     std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(states + tloc * (sw32 / 2));
-    for (std::uint32_t w = r; w < sw32; w += LPT) dst[w] = Sf[w];
+    if (PF && pa_pf) {
+      if (2 * r < sw32) reinterpret_cast<uint2*>(dst)[r] = sreg;
+    } else {
+      for (std::uint32_t w = r; w < sw32; w += LPT) dst[w] = Sf[w];
+    }
   }
   if constexpr (LANE_COUNTERS) {
     const std::uint32_t l0 = (sub * LPT) & 31;
@@ -1128,6 +1172,8 @@ kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm, bool p
 #endif
 }
 
+std::uint32_t pf_max_warps() { return kMaxWarpsPf; }
+
 std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
   return (2 * h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
 }
@@ -1167,6 +1213,15 @@ cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
+#if PBN_CARVEOUT
+  // one CTA per SM: carve out only what it takes (+1 KiB the system reserves
+  // per CTA), so that the rest of the 256 KiB stays L1 for the plan sections
+  // read through it (the perturbation cells; tables and records when unstaged)
+  err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             static_cast<int>(std::min<std::size_t>(100, (smem + 1024) * 100 / (228 * 1024) + 1)));
+  if (err != cudaSuccess) return err;
+#endif
   if (grid == 0) return cudaSuccess;
   fn<<<grid, threads, smem, stream>>>(h, d_blob, rp, d_states, d_counts);
   if (launches) ++*launches;

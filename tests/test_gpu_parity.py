@@ -239,3 +239,41 @@ def test_compact_large_network_kernel(pb, orc, cuda_ok, case):
         assert np.array_equal(cnt, ocnt)
         assert np.array_equal(st, ost)
         assert cnt[:, 6].sum() > 0  # function phases ran
+
+
+@pytest.mark.parametrize("stream", [0, 1])
+@pytest.mark.parametrize("pp", [0.0022, 0.004, 0.05])
+def test_perturbation_dominated_kernel(pb, orc, cuda_ok, stream, pp):
+    """PF kernel (p_fn < 0.02, k = 16, one phase-A block per lane): the state
+    lives in registers between function phases. Launches whose steps are
+    ~1.2 %, ~0.03 % and never function phases; predicate hits, kappa-thinned
+    transitions, the recorded series and chained launches from carried states."""
+    model, terms = pb.generate_model(2000, (1, 3), (1, 4), pp, 0.0, 2, False, 1609)
+    plan = pb.prepare(model, 1 << 25, 16, 8)
+    pred = plan.compile_predicate(terms)
+    eng = pb.GpuEnsemble(plan)
+    n, steps = 70, 700
+    tp_d = np.full(n, 2 | (1 << 2), np.uint8)
+    tp_o = tp_d.copy()
+    ser_d = np.zeros((n, 3 * steps // 32 + 2), np.uint32)
+    ser_o = ser_d.copy()
+    st_d = st_o = None
+    fn_steps = 0
+    for call in range(3):
+        st_d, c_d = eng.simulate(seed=4, n_traj=n, n_steps=steps, step_begin=call * steps,
+                                 states=st_d, pred=pred, kappa=3, thin_mode=0 if call == 0 else 1,
+                                 tprev=tp_d, series=ser_d, series_bit0=1 + call * steps,
+                                 series_init=call == 0, stream=stream)
+        if stream == 0:
+            assert "pa_prefetch" in eng.last_kernel(), eng.last_kernel()
+        st_o, c_o = orc.simulate_ex(plan.view, 4, 0, n, steps, states=st_o, step_begin=call * steps,
+                                    pred=pred, kappa=3, thin_mode=0 if call == 0 else 1,
+                                    tprev=tp_o, series=ser_o, series_bit0=1 + call * steps,
+                                    series_init=call == 0, stream=stream)
+        assert np.array_equal(c_d, c_o)
+        assert np.array_equal(st_d, st_o)
+        assert np.array_equal(tp_d, tp_o)
+        fn_steps += int(c_o[:, 6].sum())
+    assert np.array_equal(ser_d, ser_o)
+    if pp == 0.0022:
+        assert fn_steps > 500  # the store / exact function phase / reload path ran
