@@ -37,6 +37,7 @@ cudaError_t launch_ensemble_script(const dev_plan_header& h, const std::uint8_t*
                                    cudaStream_t stream);
 bool lane_kernel_fits(const dev_plan_header& h);
 std::uint32_t pf_max_warps();
+bool ensemble_pa2(const dev_plan_header& h, std::uint32_t lpt, int gm, bool pert_dom);
 int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
 std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
@@ -302,6 +303,7 @@ struct launch_choice {
   bool lane = false, scan = false;
   int gm = 0;
   bool pert_dom = false;  // sub-warp PF kernel (kPertDominated)
+  bool pa2 = false;       // sub-warp PA2 kernel (two steps per phase-A pass)
 };
 
 launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, std::uint32_t stream) {
@@ -337,6 +339,7 @@ launch_choice choose_launch(const pbn_gpu& g0, std::uint32_t n_traj, bool nc, st
   c.place = g.place;
   g.place = place0;
   c.scan = c.lane && g.p_fn < kScanBelow;
+  c.pa2 = !c.lane && ensemble_pa2(g.ep.h, c.lpt, c.gm, c.pert_dom);
   return c;
 }
 
@@ -348,6 +351,7 @@ std::string kernel_name(const launch_choice& c, std::uint32_t stream) {
   s += std::string(",stream=") + (stream == PBN_STREAM_U53 ? "u53" : "u32");
   s += std::string(",place=") + places[c.place] + ",warps=" + std::to_string(c.warps);
   if (c.pert_dom) s += ",pa_prefetch";
+  if (c.pa2) s += ",pa2";
   s += ">";
   return s;
 }

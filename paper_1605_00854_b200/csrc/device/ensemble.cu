@@ -74,10 +74,23 @@ constexpr int kPaPrefetch = PBN_PA_PREFETCH;
 #ifndef PBN_CARVEOUT
 #define PBN_CARVEOUT 1
 #endif
+#ifndef PBN_PA2
+#define PBN_PA2 1
+#endif
+constexpr bool kPa2 = PBN_PA2 != 0;
 #ifndef PBN_PF_WARPS
 #define PBN_PF_WARPS 28
 #endif
 constexpr int kMaxWarpsPf = PBN_PF_WARPS;  // PF kernels: warps per CTA (32 -> 64 registers: spills in the step loop)
+
+// PA2 (two steps per phase-A pass, see the kernel): words of the per-lane
+// pattern stash in a trajectory's shared-memory slot, 0 when the plan's phase A
+// is not the k = 16 word path filling at most half a warp. Host and device
+// size the slot with it.
+__host__ __device__ inline std::uint32_t pa2_words(const dev_plan_header& h, std::uint32_t lpt) {
+  const std::uint32_t nb0 = (h.g + h.has_leaf + 3) / 4;
+  return kPa2 && lpt == 32 && h.pert_mode == 0 && h.k == 16 && 2 * nb0 <= lpt ? 2 * lpt : 0u;
+}
 
 // One trajectory per warp runs <= 28 warps per CTA (4096 trajectories fill
 // the 148 SMs in one wave), which leaves 72 registers per thread.
@@ -87,7 +100,7 @@ constexpr int kMaxWarpsLpt32 = 28;
 // lane with shuffles (RG), 2 RG with the compact single-node records (SC), 3
 // two state words per lane (RG2, n' <= 2047) for the single-node groups
 // (general groups gather from shared memory: they run under divergence).
-template <int LPT, int STREAM, int PLACE, int GM, bool PF = false>
+template <int LPT, int STREAM, int PLACE, int GM, bool PF = false, bool PA2 = false>
 __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32) * 32 : 1024, 1)
     pbn_ensemble_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
                         const __grid_constant__ dev_run_params rp, std::uint64_t* __restrict__ states,
@@ -145,12 +158,16 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
   constexpr std::uint32_t CB = kChunkBlocks;
   constexpr std::uint32_t kBuf = LPT * 4 * CB;  // one chunk of Philox blocks (4 words)
   const std::uint32_t nc_words = rp.node_counts ? 8 * sw32 : 0u;  // counter bit-planes
-  const std::uint32_t stride = (2 * sw32 + kBuf + nc_words + 3) & ~3u;
+  // PA2 pattern stash, 8 bytes per lane (the host sizes the slots of a PA2-capable plan with it;
+  // kernels other than PA2 leave it unused)
+  constexpr std::uint32_t pa2w = PA2 ? 2u * LPT : 0u;
+  const std::uint32_t stride = (2 * sw32 + kBuf + pa2w + nc_words + 3) & ~3u;
   std::uint32_t* S0 = reinterpret_cast<std::uint32_t*>(smem + staged) +
                       static_cast<std::size_t>(slot) * stride;
   std::uint32_t* S1 = S0 + sw32;
   std::uint32_t* dbuf = S0 + 2 * sw32;  // 16-B aligned: 2*sw32 is a multiple of 4
-  std::uint32_t* planes = dbuf + kBuf;   // node counts: plane i of word w at [8*w + i]
+  std::uint32_t* pa2buf = dbuf + kBuf;   // PA2: lane r's deferred patterns at [2r], [2r+1]
+  std::uint32_t* planes = pa2buf + pa2w;  // node counts: plane i of word w at [8*w + i]
   {
     const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(states + tloc * (sw32 / 2));
     for (std::uint32_t w = r; w < sw32; w += LPT) S0[w] = src[w] & state_word_mask(h.n_kept, w);
@@ -567,8 +584,20 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     return h.has_leaf && e >= 0 && e < static_cast<int>(DPB) ? static_cast<std::uint32_t>(e) : DPB;
   };
   static_assert(DPB == 4, "phase A masks are kept as a uint4");
-  const uint4 pam0 = make_uint4(pa_mask(r, 0), pa_mask(r, 1), pa_mask(r, 2), pa_mask(r, 3));
-  const std::uint32_t lfe0 = lf_elem(r);
+  // Two steps per phase-A pass (PA2): the class of a step depends on the
+  // stream alone, so when a step's phase A fills at most half the lanes
+  // (k = 16, 2 * nb0 <= LPT; c2: 16 blocks) lanes 0..15 compute step s and
+  // lanes 16..31 step s + 1 in one pass on even steps; each step then applies
+  // its own half's patterns. Halves the phase-A Philox work per step.
+  // (PA2 kernels — a template parameter, so that they carry no other phase-A
+  // code: the hot path must stay inside the instruction cache — are the RG
+  // instantiations the host launches when pa2_words() != 0.)
+  static_assert(!PA2 || (LPT == 32 && !PF), "PA2 kernels: one trajectory per warp");
+  constexpr bool pa2 = PA2;
+  const std::uint32_t pa2_half = r / (LPT / 2 > 0 ? LPT / 2 : 1);
+  const std::uint32_t rb = pa2 ? r % (LPT / 2 > 0 ? LPT / 2 : 1) : r;  // the lane's phase-A block
+  const uint4 pam0 = make_uint4(pa_mask(rb, 0), pa_mask(rb, 1), pa_mask(rb, 2), pa_mask(rb, 3));
+  const std::uint32_t lfe0 = lf_elem(rb);
 
   // Phase-A prefetch (kPaPrefetch): lane r < nb0 fetches step s's block r and
   // the high words (U32: the words) of its four perturbation cells.
@@ -616,6 +645,8 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     return rp.pred.n != 0 && __all_sync(smask, ok) ? 1u : 0u;
   };
 
+  std::uint32_t pa2_cls = 0;  // PA2: the classes of the pass's two steps
+  step_philox spa{};          // PA2: the lane's own step's stream constants in phase A
   std::uint32_t cur = 0;
   const std::uint32_t z0 = pred_eval(S0);
   std::uint32_t prev = 2u, kphase = 0;  // previous sample (2 = none), steps since it
@@ -669,10 +700,20 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     // fill exactly state words b*WPB.., which no other lane touches: they are
     // XOR-ed in with plain read-modify-writes; otherwise per-draw atomics.
     auto phase_a_block = [&](std::uint32_t b, const uint4 pam, std::uint32_t lfe,
-                             auto bern_c, auto wpb_c) {
+                             auto bern_c, auto wpb_c, auto defer_c) {
       constexpr bool BERN = decltype(bern_c)::value;  // Method_old / Method_reduction plans
       constexpr std::uint32_t WPB = decltype(wpb_c)::value;
+      constexpr bool DEFER = decltype(defer_c)::value;  // PA2: keep the patterns, apply per step
+#ifdef PBN_SCRIPT_TU
       const uint4 x = PBN_BLK(b);
+#else
+      // PA2: the lane's own step's stream (spa: s or s + 1), else the step's
+      uint4 x;
+      if constexpr (DEFER)
+        x = philox_block(spa, b, rp.rk0, rp.rk1);
+      else
+        x = PBN_BLK(b);
+#endif
       std::uint32_t c[DPB];
       bool rare = false, lf = false;
 #pragma unroll
@@ -681,13 +722,30 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
       if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), false, 0u, rare);
       if constexpr (STREAM == STREAM_U53) {
         if (__builtin_expect(rare, 0)) {
+#ifdef PBN_SCRIPT_TU
           const uint4 y = PBN_BLK_LO(b);
+#else
+          uint4 y;
+          if constexpr (DEFER)
+            y = philox_lo_block(spa, b, rp.rk0, rp.rk1);
+          else
+            y = PBN_BLK_LO(b);
+#endif
           bool unused = false;
 #pragma unroll
           for (std::uint32_t e = 0; e < DPB; ++e)
             c[e] = pa_draw<STREAM, GP, BERN>(h, gblob, pfast, k, pick32(x, e), true, pick32(y, e), unused);
           if (lfe < DPB) lf = pa_leaf<STREAM>(h, pick32(x, lfe), true, pick32(y, lfe), unused);
         }
+      }
+      if constexpr (DEFER) {
+        static_assert(WPB == 2, "PA2 is the k = 16 word path");
+        const std::uint32_t w0 = (c[0] & pam.x) | ((c[1] & pam.y) << 16);
+        const std::uint32_t w1 = (c[2] & pam.z) | ((c[3] & pam.w) << 16);
+        reinterpret_cast<uint2*>(pa2buf)[r] = make_uint2(w0, w1);  // read back by this lane only
+        flip = (w0 | w1) != 0;
+        leaf = lf;
+        return;
       }
       leaf = leaf || lf;
       if constexpr (WPB == 2) {  // k = 16: elements 0,1 -> word 2b, elements 2,3 -> word 2b+1
@@ -758,28 +816,55 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     };
     auto phase_a = [&](auto bern_c, auto wpb_c) {
       if (nb0 <= LPT) {  // launch-uniform: at most one block per lane (masks precomputed)
-        if (r < nb0) phase_a_block(r, pam0, lfe0, bern_c, wpb_c);
+        if (r < nb0) phase_a_block(r, pam0, lfe0, bern_c, wpb_c, std::false_type{});
       } else {
         for (std::uint32_t b = r; b < nb0; b += LPT)
           phase_a_block(b, make_uint4(pa_mask(b, 0), pa_mask(b, 1), pa_mask(b, 2), pa_mask(b, 3)),
-                        lf_elem(b), bern_c, wpb_c);
+                        lf_elem(b), bern_c, wpb_c, std::false_type{});
       }
     };
-    if (PF && pa_pf) {  // launch-uniform
-      if (r < nb0) {
-        phase_a_prefetched();
-        if constexpr (kPaPrefetch == 1) pa_fetch(s + 1);
+    bool any_flip, any_leaf;
+    if constexpr (PA2) {
+      const std::uint32_t j = static_cast<std::uint32_t>(s - rp.step_begin) & 1u;
+      if (j == 0) {  // both steps' blocks: lanes 0..15 step s, lanes 16..31 step s + 1
+        spa = make_step_philox(thi0, tlo0, s + pa2_half, rp.rk0, rp.rk1);
+        if (rb < nb0)
+          phase_a_block(rb, pam0, lfe0, std::false_type{}, std::integral_constant<std::uint32_t, 2>{},
+                        std::true_type{});
+        // the two steps' classes: bit j = step s + j has a kept flip, bit 2 + j = its leaf fired
+        const std::uint32_t fm = __ballot_sync(smask, flip), lm = __ballot_sync(smask, leaf);
+        pa2_cls = ((fm & 0xFFFFu) ? 1u : 0u) | ((fm >> 16) ? 2u : 0u) | ((lm & 0xFFFFu) ? 4u : 0u) |
+                  ((lm >> 16) ? 8u : 0u);
       }
-    } else if (h.pert_mode != 0)  // plan-uniform
-      phase_a(std::true_type{}, std::integral_constant<std::uint32_t, 0>{});
-    else if (k == 16)
-      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 2>{});
-    else if (k == 8)
-      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 1>{});
-    else
-      phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 0>{});
-    const bool any_flip = __ballot_sync(smask, flip) != 0;
-    const bool any_leaf = __ballot_sync(smask, leaf) != 0;
+      any_flip = ((pa2_cls >> j) & 1u) != 0;
+      any_leaf = ((pa2_cls >> (2 + j)) & 1u) != 0;
+      if (any_flip && pa2_half == j && rb < nb0) {
+        const uint2 pw = reinterpret_cast<const uint2*>(pa2buf)[r];
+        if ((pw.x | pw.y) != 0) {  // xor_chunk (bitstate.hpp:50-58)
+          uint2* w = reinterpret_cast<uint2*>(Sc) + rb;
+          uint2 v = *w;
+          v.x ^= pw.x;
+          v.y ^= pw.y;
+          *w = v;
+        }
+      }
+    } else {
+      if (PF && pa_pf) {  // launch-uniform
+        if (r < nb0) {
+          phase_a_prefetched();
+          if constexpr (kPaPrefetch == 1) pa_fetch(s + 1);
+        }
+      } else if (h.pert_mode != 0)  // plan-uniform
+        phase_a(std::true_type{}, std::integral_constant<std::uint32_t, 0>{});
+      else if (k == 16)
+        phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 2>{});
+      else if (k == 8)
+        phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 1>{});
+      else
+        phase_a(std::false_type{}, std::integral_constant<std::uint32_t, 0>{});
+      any_flip = __ballot_sync(smask, flip) != 0;
+      any_leaf = __ballot_sync(smask, leaf) != 0;
+    }
 
     std::uint32_t ev = 0;  // this step's events (LANE_COUNTERS bit layout)
     if (any_flip) {
@@ -1118,24 +1203,24 @@ __global__ void pbn_philox_kat_kernel(const uint4* ctr, std::uint32_t k0, std::u
 using kernel_fn = void (*)(const dev_plan_header, const std::uint8_t*, const dev_run_params,
                            std::uint64_t*, std::uint64_t*);
 
-template <int LPT, int STREAM, int GM>
+template <int LPT, int STREAM, int GM, bool PA2 = false>
 kernel_fn pick_place(int place) {
   switch (place) {
     case PLACE_ALL:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, GM>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_ALL, GM, false, PA2>;
     case PLACE_CORE_PERT:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE_PERT, GM>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE_PERT, GM, false, PA2>;
     case PLACE_TABLES:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, GM>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_TABLES, GM, false, PA2>;
     case PLACE_CORE:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, GM>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_CORE, GM, false, PA2>;
     default:
-      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL, GM>;
+      return pbn_ensemble_kernel<LPT, STREAM, PLACE_GLOBAL, GM, false, PA2>;
   }
 }
 
 template <int STREAM>
-kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
+kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm, bool pa2) {
   switch (lpt) {
     case 1:
       return pick_place<1, STREAM, 0>(place);
@@ -1150,6 +1235,8 @@ kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
     default:
       if constexpr (STREAM == STREAM_U53)
         if (gm == 4) return pick_place<32, STREAM, 4>(place);
+      if (pa2 && gm == 2) return pick_place<32, STREAM, 2, true>(place);
+      if (pa2 && gm == 1) return pick_place<32, STREAM, 1, true>(place);
       return gm == 3   ? pick_place<32, STREAM, 3>(place)
              : gm == 2 ? pick_place<32, STREAM, 2>(place)
              : gm == 1 ? pick_place<32, STREAM, 1>(place)
@@ -1157,25 +1244,26 @@ kernel_fn pick_lpt(std::uint32_t lpt, int place, int gm) {
   }
 }
 
-kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm, bool pert_dom) {
+kernel_fn select_kernel(std::uint32_t lpt, int stream, int place, int gm, bool pert_dom, bool pa2) {
 #ifdef PBN_FAST_BUILD  // register-allocation experiments: the headline instantiations only
   if (pert_dom) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 0, true>;
   if (gm == 4) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 4>;
   if (gm == 0) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_CORE, 0>;
+  if (pa2) return pbn_ensemble_kernel<32, STREAM_U53, PLACE_TABLES, 2, false, true>;
   return pbn_ensemble_kernel<32, STREAM_U53, PLACE_TABLES, 2>;
 #else
   if (pert_dom)  // perturbation-dominated launch: plan through L1/L2, phase-A prefetch
     return stream == STREAM_U53 ? pbn_ensemble_kernel<32, STREAM_U53, PLACE_GLOBAL, 0, true>
                                 : pbn_ensemble_kernel<32, STREAM_U32, PLACE_GLOBAL, 0, true>;
-  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, gm)
-                              : pick_lpt<STREAM_U32>(lpt, place, gm);
+  return stream == STREAM_U53 ? pick_lpt<STREAM_U53>(lpt, place, gm, pa2)
+                              : pick_lpt<STREAM_U32>(lpt, place, gm, pa2);
 #endif
 }
 
 std::uint32_t pf_max_warps() { return kMaxWarpsPf; }
 
 std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts) {
-  return (2 * h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
+  return (2 * h.sw32 + lpt * 4 * kChunkBlocks + pa2_words(h, lpt) + (node_counts ? 8 * h.sw32 : 0) + 3) & ~3u;
 }
 
 // Parent gather mode of the sub-warp kernel for a plan (GM template
@@ -1194,13 +1282,19 @@ int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream
   return rg2 ? 3 : !rg ? 0 : (h.single_compact && kUseCompactSingle) ? 2 : 1;
 }
 
+// Two-steps-per-pass phase A (PA2 kernels): the register-gather kernels on a
+// plan whose phase A is the k = 16 word path over at most half a warp.
+bool ensemble_pa2(const dev_plan_header& h, std::uint32_t lpt, int gm, bool pert_dom) {
+  return !pert_dom && (gm == 1 || gm == 2) && pa2_words(h, lpt) != 0;
+}
+
 cudaError_t launch_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
                             int stream_kind, std::uint32_t lpt, std::uint32_t warps_per_cta,
                             const dev_run_params& rp, std::uint64_t* d_states,
                             std::uint64_t* d_counts, cudaStream_t stream,
                             std::uint32_t* launches, bool pert_dom) {
   const int gm = pert_dom ? 0 : ensemble_gather_mode(h, lpt, stream_kind);
-  const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm, pert_dom);
+  const kernel_fn fn = select_kernel(lpt, stream_kind, place, gm, pert_dom, ensemble_pa2(h, lpt, gm, pert_dom));
   const std::uint32_t threads = warps_per_cta * 32;
   const std::uint32_t slots = threads / lpt;
   const std::uint32_t grid = (rp.n_traj + slots - 1) / slots;
