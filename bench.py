@@ -648,8 +648,8 @@ def run_ours(a):
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_lookups,
                      "unit": "lookups/s", "frac": achieved / peak_lookups, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-                     "issue_bound_evidence": "profiles/r02_c2_u53.txt: issue slots ~68% "
-                                             "busy, ALU pipe ~67%, smem wavefronts ~52% of peak",
+                     "issue_bound_evidence": "profiles/r02_c2_u53.txt: issue slots ~72% "
+                                             "busy, ALU pipe ~71%, smem wavefronts ~57% of peak",
                      "note": "lookup roofline = SMs x 32 probes/clk x sm_max_mhz "
                              "(MEASURED_PEAKS.json); algorithmic lookups = g per step + "
                              "(A+G) per function-phase step (SURVEY 8d), per GPU",

@@ -37,10 +37,11 @@ cudaError_t launch_ensemble_script(const dev_plan_header& h, const std::uint8_t*
                                    cudaStream_t stream);
 bool lane_kernel_fits(const dev_plan_header& h);
 std::uint32_t pf_max_warps();
+std::size_t slot_words(const dev_plan_header& h, std::uint32_t lpt, bool node_counts);
 bool ensemble_pa2(const dev_plan_header& h, std::uint32_t lpt, int gm, bool pert_dom);
 int ensemble_gather_mode(const dev_plan_header& h, std::uint32_t lpt, int stream);
 std::uint32_t lane_max_warps();
-std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts);
+std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts, bool scan);
 const char* lane_rare_fn_name();
 std::size_t lane_cta_bytes();
 cudaError_t launch_philox_kat(const uint4* d_ctr, std::uint32_t k0, std::uint32_t k1, uint4* d_out,
@@ -224,7 +225,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
     const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) + 31) / 32;
     std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
     w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lane_max_warps(), w));
-    const std::uint64_t per_warp = lane_warp_words(g.ep.h, node_counts) * 4;
+    const std::uint64_t per_warp = lane_warp_words(g.ep.h, node_counts, g.p_fn < kScanBelow) * 4;
     const std::uint64_t avail = g.smem_optin - staged_bytes(g) - lane_cta_bytes() - 64;
     while (w > 1 && w * per_warp > avail) --w;
     if (w * per_warp > avail) throw resource_error("trajectory state does not fit in shared memory");
@@ -233,8 +234,7 @@ std::uint32_t pick_warps(const pbn_gpu& g, std::uint32_t n_traj, std::uint32_t l
   const std::uint64_t warps_needed = (static_cast<std::uint64_t>(n_traj) * lpt + 31) / 32;
   std::uint64_t w = (warps_needed + g.sms - 1) / g.sms;
   w = std::max<std::uint64_t>(1, std::min<std::uint64_t>(lpt == 32 ? max_warps_lpt32 : 32, w));
-  const std::uint64_t stride =
-      (2 * g.ep.h.sw32 + lpt * 4 * kChunkBlocks + (node_counts ? 8 * g.ep.h.sw32 : 0) + 3) & ~3u;
+  const std::uint64_t stride = slot_words(g.ep.h, lpt, node_counts);  // the launcher's own size
   const std::uint64_t per_warp = static_cast<std::uint64_t>(32 / lpt) * stride * 4;
   const std::uint64_t avail = g.smem_optin - std::max(staged_bytes(g), min_staged) - 64;
   while (w > 1 && w * per_warp > avail) --w;

@@ -55,7 +55,12 @@ constexpr int kScanFnLanes = PBN_SCAN_FN_LANES;
 // phase (pays when the function phase is rare, c1); otherwise all lanes take
 // step s together and the function phase runs under divergence (c3, where
 // ~90% of steps reach it).
-// MODE 0 lockstep, 1 scan-ahead (SCAN), 2 CTA-compacted function phases.
+// MODE 0 lockstep, 1 scan-ahead (SCAN), 2 CTA-compacted function phases,
+// 3 scan-ahead with a per-lane queue of precomputed phase-A steps (QUEUE).
+#ifndef PBN_LANE_QUEUE
+#define PBN_LANE_QUEUE 4
+#endif
+constexpr std::uint32_t kQueueDepth = PBN_LANE_QUEUE;
 template <int STREAM, int PLACE, int MODE>
 __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
     pbn_lane_kernel(const __grid_constant__ dev_plan_header h, const std::uint8_t* __restrict__ gblob,
@@ -96,7 +101,8 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   // per-warp shared memory: two state buffers of sw32 words x 32 lanes, then
   // (node counts) 8 counter planes per word; lane columns
   const std::uint32_t sw32 = h.sw32;
-  const std::uint32_t warp_words = (2 + (rp.node_counts ? 8u : 0u)) * sw32 * 32;
+  const std::uint32_t warp_words =
+      (2 + (rp.node_counts ? 8u : 0u) + (MODE == 3 ? kQueueDepth : 0u)) * sw32 * 32;
   std::uint32_t* wbuf = reinterpret_cast<std::uint32_t*>(smem + staged) +
                         static_cast<std::size_t>(warp) * warp_words + lane;
   std::uint32_t* planes = wbuf + 2 * sw32 * 32;  // plane i of word w at [(8w + i) * 32]
@@ -453,6 +459,68 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
         step_stats(wbuf + cur * (sw32 * 32), s);
       }
     }
+  } else if constexpr (MODE == 3) {
+    // QUEUE: the class of a step AND its flip patterns depend on the stream
+    // only, so a lane whose next step needs the function phase keeps
+    // producing: phase A of its following steps goes into a queue of up to
+    // kQueueDepth (XOR mask, class) entries in shared memory ([slot][word]
+    // [lane] columns) instead of waiting for the warp. Three kinds of rounds:
+    // consume — every lane applies its queued perturbed / leaf steps up to its
+    // next function-phase step (a few XORs + the statistics); function — run
+    // by the warp once >= kScanFnLanes lanes have one at the head of their
+    // queue (or nothing can be produced); produce — every lane with room
+    // computes phase A of its next unqueued step. The expensive rounds
+    // (produce: Philox + cell probes; function: the group loop) both run with
+    // nearly full warps.
+    std::uint32_t* qbuf = wbuf + (2 + (rp.node_counts ? 8u : 0u)) * sw32 * 32;
+    std::uint64_t s = rp.step_begin;  // the lane's next step to take (head of the queue)
+    std::uint32_t qn = 0;             // queued steps s .. s + qn - 1
+    std::uint32_t qcls = 0;           // their classes, 2 bits each, head in bits 0-1: 0 flip, 1 leaf, 2 function
+    std::uint32_t qhead = 0;          // slot of the head
+    for (;;) {
+      while (qn != 0 && (qcls & 3u) != 2u) {  // consume
+        std::uint32_t* Sc = wbuf + cur * (sw32 * 32);
+        if ((qcls & 3u) == 0u) {
+          const std::uint32_t* q = qbuf + qhead * (sw32 * 32);
+          for (std::uint32_t w = 0; w < sw32; ++w) Sc[32 * w] ^= q[32 * w];
+          ++npert;
+        }
+        step_stats(Sc, s);
+        ++s;
+        qcls >>= 2;
+        --qn;
+        qhead = qhead + 1 == kQueueDepth ? 0u : qhead + 1;
+      }
+      const bool fn_head = qn != 0;  // its class is 2 after the consume loop
+      const bool can_produce = qn < kQueueDepth && s + qn < s_end;
+      const std::uint32_t pend = __ballot_sync(lmask, fn_head);
+      const std::uint32_t prod = __ballot_sync(lmask, can_produce);
+      if (pend == 0 && prod == 0) break;
+      if (prod == 0 || __popc(pend) >= kScanFnLanes) {
+        if (fn_head) {
+          const step_philox sp = make_step_philox(thi0, tlo0, s, rp.rk0, rp.rk1);
+          std::uint32_t* Sn = wbuf + (cur ^ 1) * (sw32 * 32);
+          fn_phase(wbuf + cur * (sw32 * 32), Sn, sp);
+          cur ^= 1;
+          ++nfn;
+          step_stats(Sn, s);
+          ++s;
+          qcls >>= 2;
+          --qn;
+          qhead = qhead + 1 == kQueueDepth ? 0u : qhead + 1;
+        }
+      } else if (can_produce) {
+        std::uint32_t slot = qhead + qn;
+        if (slot >= kQueueDepth) slot -= kQueueDepth;
+        std::uint32_t* q = qbuf + slot * (sw32 * 32);
+        for (std::uint32_t w = 0; w < sw32; ++w) q[32 * w] = 0;
+        const step_philox sp = make_step_philox(thi0, tlo0, s + qn, rp.rk0, rp.rk1);
+        bool flip, leaf;
+        phase_a_step(q, sp, flip, leaf);
+        qcls |= (flip ? 0u : leaf ? 1u : 2u) << (2 * qn);
+        ++qn;
+      }
+    }
   } else if constexpr (SCAN) {
     // The class of a step (perturbed / leaf no-op / function phase) depends
     // on the stream only, never on the state: each lane scans its own steps
@@ -560,8 +628,16 @@ lane_kernel_fn pick_lane_place(int place) {
 #ifndef PBN_LANE_COMPACT
 #define PBN_LANE_COMPACT 0
 #endif
-constexpr int kRareFnMode = PBN_LANE_COMPACT ? 2 : 1;
-const char* lane_rare_fn_name() { return kRareFnMode == 2 ? "compact" : "scan"; }
+// QUEUE (3) is bit-exact and cuts the produce rounds from 2.09 to 1.39 per
+// step on c1, but its consume rounds and stash traffic cost more than that
+// saves: 9.24e9 vs 9.49e9 trajectory-steps/s for SCAN.
+#ifndef PBN_LANE_RARE_MODE
+#define PBN_LANE_RARE_MODE 1
+#endif
+constexpr int kRareFnMode = PBN_LANE_COMPACT ? 2 : PBN_LANE_RARE_MODE;
+const char* lane_rare_fn_name() {
+  return kRareFnMode == 2 ? "compact" : kRareFnMode == 3 ? "queue" : "scan";
+}
 // Shared memory of the CTA-compaction variant: warp counts + the task list.
 std::size_t lane_cta_bytes() { return kRareFnMode == 2 ? 4 * 32 + 2 * 32 * kLaneMaxWarps + 16 : 0; }
 
@@ -572,8 +648,9 @@ std::uint32_t lane_max_warps() { return kLaneMaxWarps; }
 
 // Shared-memory words per warp of the lane kernel: two state buffers and the
 // optional counter planes, sw32 words per lane each.
-std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts) {
-  return static_cast<std::size_t>(2 + (node_counts ? 8 : 0)) * h.sw32 * 32;
+std::size_t lane_warp_words(const dev_plan_header& h, bool node_counts, bool scan) {
+  return static_cast<std::size_t>(2 + (node_counts ? 8 : 0) +
+                                  (scan && kRareFnMode == 3 ? kQueueDepth : 0)) * h.sw32 * 32;
 }
 
 cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d_blob, int place,
@@ -591,7 +668,7 @@ cudaError_t launch_lane_ensemble(const dev_plan_header& h, const std::uint8_t* d
                                                       : staged_prefix<STREAM_U32>(h, place);
   const std::size_t smem = staged +
                            static_cast<std::size_t>(warps_per_cta) *
-                               lane_warp_words(h, rp.node_counts != nullptr) * 4 +
+                               lane_warp_words(h, rp.node_counts != nullptr, scan) * 4 +
                            (scan ? lane_cta_bytes() : 0) + 16;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,

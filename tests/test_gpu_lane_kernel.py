@@ -157,3 +157,38 @@ def test_auto_selection_large_ensemble(pb, orc, cuda_ok):
     assert eng.info()["lanes_per_traj"] == 1
     ost, ocnt = orc.simulate(plan.view, 6, 0, n, 40, pred=pred)
     assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt)
+
+
+@pytest.mark.parametrize("case", ["c1", "c1_k16", "n64"])
+@pytest.mark.parametrize("stream", [0, 1])
+def test_lane_kernel_queue_mode_statistics(pb, orc, cuda_ok, case, stream):
+    """The rare-function-phase variant (per-lane queue of precomputed phase-A
+    steps): thinned transitions, series, node counts and chained launches —
+    queued steps never cross a launch, the statistics follow consume order."""
+    plan, pred = _setup(pb, case)
+    eng = pb.GpuEnsemble(plan, lanes_per_traj=1)
+    n, steps = 200, 517
+    tp_d = np.full(n, 2 | (1 << 2), np.uint8)
+    tp_o = tp_d.copy()
+    ser_d = np.zeros((n, 3 * steps // 32 + 2), np.uint32)
+    ser_o = ser_d.copy()
+    st_d = st_o = None
+    for call in range(3):
+        st_d, c_d = eng.simulate(seed=11, n_traj=n, n_steps=steps, step_begin=call * steps,
+                                 states=st_d, pred=pred, kappa=3,
+                                 thin_mode=0 if call == 0 else 1, tprev=tp_d, series=ser_d,
+                                 series_bit0=1 + call * steps, series_init=call == 0, stream=stream)
+        assert eng.last_kernel().startswith("lane<queue") or eng.last_kernel().startswith("lane<scan"), \
+            eng.last_kernel()
+        st_o, c_o = orc.simulate_ex(plan.view, 11, 0, n, steps, states=st_o,
+                                    step_begin=call * steps, pred=pred, kappa=3,
+                                    thin_mode=0 if call == 0 else 1, tprev=tp_o,
+                                    series=ser_o, series_bit0=1 + call * steps,
+                                    series_init=call == 0, stream=stream)
+        assert np.array_equal(c_d, c_o)
+        assert np.array_equal(st_d, st_o)
+        assert np.array_equal(tp_d, tp_o)
+    assert np.array_equal(ser_d, ser_o)
+    st, cnt, nc = eng.simulate(seed=8, n_traj=100, n_steps=700, pred=pred, node_counts=True, stream=stream)
+    ost, ocnt, onc = orc.simulate(plan.view, 8, 0, 100, 700, pred=pred, node_counts=True, stream=stream)
+    assert np.array_equal(st, ost) and np.array_equal(cnt, ocnt) and np.array_equal(nc, onc)
