@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     rare = false;
     if constexpr (SCL) {
       // sgrp cells (dev_plan.h): the choice on the high word's top 28 bits
-      const uint4 R = sgrp[j];
+      const uint4 R = lds128(sgrp + j);  // always staged (GM 4)
       const std::uint32_t hi = dbuf[jj];
       const std::uint32_t N = (R.x & 3u) + 1u;
       const std::uint64_t P = static_cast<std::uint64_t>(hi) * N;

@@ -62,6 +62,18 @@ __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// One 16-byte shared-memory load that stays one LDS.128 (4 wavefronts per
+// warp for consecutive records). Left to the compiler, a uint4 record whose
+// components are consumed one by one under selects is split into 4-byte
+// loads at a 16-byte lane stride — 4-way bank conflicts on each.
+__device__ __forceinline__ uint4 lds128(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 // Stage bytes [0, n0) of the blob, then (n1 > 0) n1 bytes from src1 right
 // after them, with bulk copies (multiples of 16 bytes) completing on one
 // mbarrier; every thread of the CTA waits.
