@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     pfx = philox_block(spn, r, rp.rk0, rp.rk1);
     auto cell = [&](std::uint32_t hw) -> std::uint32_t {
       if constexpr (STREAM == STREAM_U53)
-        return pert53_hi_word<GP>(pfast, hw >> 16);
+        return pert53_hi_word<GP, false>(pfast, hw >> 16);
       else
         return ldp<GP>(reinterpret_cast<const std::uint32_t*>(pfast) + (hw >> 16));
     };

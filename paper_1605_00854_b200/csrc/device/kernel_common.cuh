@@ -209,13 +209,29 @@ __device__ __forceinline__ const std::uint8_t* pert_fast_base(const std::uint8_t
   else
     return pcells;
 }
+#ifndef PBN_PERT_NOALLOC
+#define PBN_PERT_NOALLOC 1
+#endif
 // The high word of U53 cell c.
-template <bool G>
+// NA (no L1 allocation): the random 4-byte probes of the 256 KiB table go
+// through L2 without taking L1 lines from the plan sections that do get
+// reused (+0.4-0.5 % on c2/c4/c5 p <= 1e-3); the PF kernels, where these
+// probes are all there is, keep them in L1 (34 % hits; without: -40 %).
+template <bool G, bool NA = true>
 __device__ __forceinline__ std::uint32_t pert53_hi_word(const std::uint8_t* pfast, std::uint32_t c) {
-  if constexpr (G && kPert53h)
-    return __ldg(reinterpret_cast<const std::uint32_t*>(pfast) + c);
-  else
+  if constexpr (G && kPert53h) {
+    if constexpr (NA && PBN_PERT_NOALLOC != 0) {
+      std::uint32_t v;
+      asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];"
+          : "=r"(v)
+          : "l"(reinterpret_cast<const std::uint32_t*>(pfast) + c));
+      return v;
+    } else {
+      return __ldg(reinterpret_cast<const std::uint32_t*>(pfast) + c);
+    }
+  } else {
     return ldp<G>(reinterpret_cast<const std::uint32_t*>(pfast) + 2 * c + 1);
+  }
 }
 // The full 8-byte U53 cells (the exact paths): not kept in a register by G
 // launches (the header and the blob pointer are kernel parameters).
