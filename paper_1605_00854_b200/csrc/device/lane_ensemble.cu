@@ -151,11 +151,26 @@ __global__ void __launch_bounds__(kLaneMaxWarps * 32, 1)
   auto gather_fn = [&](const std::uint32_t* S, const uint4& F) -> std::uint32_t {
     const std::uint32_t gc = F.y & 31u;
     std::uint32_t v = gather4_col(S, F.z, F.w, 0);
-    if (gc > 4) {
+    if constexpr (MODE == 0) {
+      // lockstep (c3: most chosen functions have more than four inputs): the loop form
+      if (gc > 4) {
+        const std::uint32_t xq = F.y >> 8;
+        for (std::uint32_t q = 4; q < gc; q += 4) {
+          const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+          v |= gather4_col(S, rr.x, rr.y, q);
+        }
+      }
+    } else if (gc > 4) {
+      // scan-ahead variants (c1: few do): inputs 4..7 without a loop; measured
+      // per instantiation — c1 9.49e9 -> 1.04e10, while c3 loses 3.7 % with this form
       const std::uint32_t xq = F.y >> 8;
-      for (std::uint32_t q = 4; q < gc; q += 4) {
-        const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
-        v |= gather4_col(S, rr.x, rr.y, q);
+      const uint2 r4 = ldp<GC>(grec + xq);
+      v |= gather4_col(S, r4.x, r4.y, 4);
+      if (__builtin_expect(gc > 8, 0)) {
+        for (std::uint32_t q = 8; q < gc; q += 4) {
+          const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+          v |= gather4_col(S, rr.x, rr.y, q);
+        }
       }
     }
     return v;
