@@ -74,6 +74,9 @@ constexpr int kPaPrefetch = PBN_PA_PREFETCH;
 #ifndef PBN_CARVEOUT
 #define PBN_CARVEOUT 1
 #endif
+#ifndef PBN_GATHER_UNROLL
+#define PBN_GATHER_UNROLL 1
+#endif
 #ifndef PBN_PA2
 #define PBN_PA2 1
 #endif
@@ -274,10 +277,22 @@ __global__ void __launch_bounds__(LPT == 32 ? (PF ? kMaxWarpsPf : kMaxWarpsLpt32
     std::uint32_t v = gather4(Sc, F.z, F.w, 0);
     if (gc > 4) {
       const std::uint32_t xq = F.y >> 8;
+#if PBN_GATHER_UNROLL
+      // inputs 4..7 without the per-lane loop (up to 8 inputs: every
+      // max_group_parents <= 8 plan); the loop only for wider functions
+      const uint2 r4 = ldp<GC>(grec + xq);
+      v |= gather4(Sc, r4.x, r4.y, 4);
+      if (__builtin_expect(gc > 8, 0))
+        for (std::uint32_t q = 8; q < gc; q += 4) {
+          const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
+          v |= gather4(Sc, rr.x, rr.y, q);
+        }
+#else
       for (std::uint32_t q = 4; q < gc; q += 4) {
         const uint2 rr = ldp<GC>(grec + xq + ((q - 4) >> 2));
         v |= gather4(Sc, rr.x, rr.y, q);
       }
+#endif
     }
     return v;
   };
